@@ -1,0 +1,330 @@
+"""Benchmark of the hot path: Phi over a batch of word-RASP machines.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): per GPU, 2^20 synthetic
+programs from generator G (seed = rank), w=16, n=64, ell=8, s=8, run to halt
+with a 1024-step cap.  Each rank runs its own shard (weak scaling; the only
+collective is the all-reduce of the 102-bucket halting histogram).
+
+One "step" = one full run of the batch from c0 (out-of-place, c0 is never
+modified) plus the on-device halting histogram.  Metric: machine-steps/s
+(sum of per-machine applied steps, hypervisor.py:153, over all ranks / max
+per-rank device time).
+
+--impl reference times the reference algorithm on the host cores instead:
+the C restatement of _worker (oracle/rasp_oracle.c, hv:72-164) driven with
+the reference's striped thread schedule (hv:295-314) over all host threads,
+on a bounded sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (d per GPU, w, n, ell, s, tau_max, description)
+    "c1": (4096, 8, 32, 4, 4, 64, "4096 random programs, w=8 n=32 l=4 s=4, 64 steps"),
+    "c2": (1 << 20, 16, 64, 8, 8, 1024,
+           "1M random programs/GPU, w=16 n=64 l=8 s=8, run to halt (cap 1024)"),
+    "c3": (1 << 24, 16, 64, 8, 8, 1024,
+           "16M random programs/GPU, w=16 n=64 l=8 s=8, run to halt (cap 1024)"),
+    "c5": (1 << 20, 32, 256, 32, 32, 1024,
+           "1M random programs/GPU, w=32 n=256 l=32 s=32, divergent halting (cap 1024)"),
+}
+N_ALG_INSTR = 40   # algorithmic integer issues per machine-step
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), float(pk.get("sm_max_mhz", 1965.0)), "measured"
+    except Exception:
+        return 6650.0, 1965.0, "fallback"
+
+
+def s_alg_bytes(w, n, ell, s):
+    bw = 1 if w <= 8 else 2 if w <= 16 else 4 if w <= 32 else 8
+    return (n + ell + s + 4) * bw + 8
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_reference(cfg_name, steps_k, warmup, sample_d=None, seed=0):
+    """Time the reference algorithm on the host (oracle port, all threads)."""
+    from oracle import oracle
+    from paper_2604_12902_b200.machine import MachineParams
+    from paper_2604_12902_b200.workload import synthetic_c0
+    d, w, n, ell, s, tau, _ = CONFIGS[cfg_name]
+    sample = min(d, sample_d or (1 << 16))
+    p = MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
+    c0 = synthetic_c0(sample, p, seed=seed)
+    cores = len(os.sched_getaffinity(0))
+    oracle.load()
+    times, steps_total = [], 0
+    for it in range(warmup + steps_k):
+        t0 = time.perf_counter()
+        out = oracle.worker_arrays(c0, w, n, ell, s, tau, epoch=64, workers=cores)
+        dt = time.perf_counter() - t0
+        if it >= warmup:
+            times.append(dt)
+            steps_total = int(out["steps"].sum())
+    best = min(times) if times else float("nan")
+    return {"value": steps_total / best, "unit": "machine-steps/s", "cores": cores,
+            "kind": "port", "sample": f"{sample} machines of {cfg_name} (generator G seed {seed}), "
+            f"{steps_total} machine-steps, _worker semantics, W={cores} threads, q=64, "
+            f"best of {len(times)}", "seconds": best}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--epoch", type=int, default=32)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 16)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    d, w, n, ell, s, tau, desc = CONFIGS[args.config]
+    metric = "machine-steps/s"
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        cb = cpu_reference(args.config, max(args.steps, 1), max(args.warmup, 0) and 1,
+                           args.cpu_sample)
+        line = {
+            "metric": metric, "value": cb["value"], "unit": "machine-steps/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "u64", "data": "synthetic (generator G)",
+            "config": {"workload": args.config, "desc": desc, "w": w, "n": n, "ell": ell, "s": s,
+                       "tau_max": tau, "d_sample": min(d, args.cpu_sample)},
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": "machine-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line))
+        return
+
+    import torch
+    import torch.distributed as dist
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2604_12902_b200 import _native
+    from paper_2604_12902_b200.engine import DeviceBatch
+    from paper_2604_12902_b200.hypervisor import get_engine
+    from paper_2604_12902_b200.machine import MachineParams
+    from paper_2604_12902_b200.workload import synthetic_c0
+
+    p = MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
+    host = synthetic_c0(d, p, seed=rank)
+    eng = get_engine(p, dev)
+    lib = _native.load()
+    src = DeviceBatch.from_arrays(host, p, dev)
+    dst = DeviceBatch.empty(d, p, dev, fresh=False)
+    hist = torch.empty(102, dtype=torch.int64, device=dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+    stream = torch.cuda.current_stream(dev)
+
+    def one_step():
+        eng.run(src, tau, args.epoch, out=dst, fresh=True, stream=stream)
+        eng.histogram(dst, out=hist, stream=stream)
+        if world > 1:
+            dist.all_reduce(hist)
+
+    for _ in range(max(args.warmup, 0)):
+        one_step()
+    torch.cuda.synchronize()
+    machine_steps = int(dst.steps.sum().item())
+    halted = int((dst.status == 1).sum().item())
+
+    # --- timed region: device time per step with CUDA events; L2 flushed between steps
+    clocks = ClockSampler(local_rank)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches0 = lib.rasp_launch_count()
+    t_wall0 = time.perf_counter()
+    evs = []
+    for _ in range(args.steps):
+        flush.fill_(1)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        one_step()
+        e1.record(stream)
+        evs.append((e0, e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    wall = time.perf_counter() - t_wall0
+    launches = lib.rasp_launch_count() - launches0
+    clk = clocks.stop()
+    per_step = [a.elapsed_time(b) / 1e3 for a, b in evs]
+    t_step = statistics.mean(per_step)
+    # kernel-only time of rasp_run (dominant kernel: the epoch kernel)
+    k0 = torch.cuda.Event(enable_timing=True)
+    k1 = torch.cuda.Event(enable_timing=True)
+    kt = []
+    for _ in range(max(3, min(args.steps, 5))):
+        flush.fill_(1)
+        k0.record(stream)
+        eng.run(src, tau, args.epoch, out=dst, fresh=True, stream=stream)
+        k1.record(stream)
+        k1.synchronize()
+        kt.append(k0.elapsed_time(k1) / 1e3)
+    t_kernel = statistics.mean(kt)
+
+    # --- e2e through the public API with host buffers (pinned), copies inside
+    from paper_2604_12902_b200.pipeline import HostPipeline
+    pipe = HostPipeline(p, d, dev, engine=eng)
+    pin_in = pipe.pinned_inputs(host)
+    e2e_times = []
+    for it in range(args.warmup + args.steps):
+        t = pipe.run(pin_in, tau, args.epoch)
+        if it >= args.warmup:
+            e2e_times.append(t)
+    t_e2e = statistics.mean(e2e_times)
+    out_np = pipe.results()
+    assert int(out_np["steps"].astype(np.int64).sum()) == machine_steps
+
+    if world > 1:
+        tt = torch.tensor([t_step, t_kernel, t_e2e, machine_steps, halted], dtype=torch.float64,
+                          device=dev)
+        mx = tt[:3].clone()
+        sm = tt[3:].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        t_step, t_kernel, t_e2e = (float(v) for v in mx.tolist())
+        total_steps, total_halted = (int(v) for v in sm.tolist())
+    else:
+        total_steps, total_halted = machine_steps, halted
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    hbm_gbs, sm_mhz, peak_kind = _peaks()
+    value = total_steps / t_step
+    bytes_alg = d * 2 * s_alg_bytes(w, n, ell, s)          # per GPU, per launch set
+    issue_peak = 148 * 4 * 32 * sm_mhz * 1e6                 # thread-instr/s
+    ach_issue = machine_steps * N_ALG_INSTR / t_kernel
+    roof = {
+        "bound": "issue", "unit": "Tinstr/s",
+        "achieved": ach_issue / 1e12, "peak": issue_peak / 1e12,
+        "frac": ach_issue / issue_peak, "traffic": None,
+        "per_unit": f"{N_ALG_INSTR} int-instr per machine-step (SURVEY §8d)",
+        "peak_source": f"148 SM x 128 lanes x {sm_mhz:.0f} MHz ({peak_kind} sm_max_mhz)",
+        "hbm": {"achieved": bytes_alg / t_kernel / 1e9, "peak": hbm_gbs, "unit": "GB/s",
+                "frac": bytes_alg / t_kernel / 1e9 / hbm_gbs,
+                "per_unit": f"S_alg={s_alg_bytes(w, n, ell, s)} B/machine read+write",
+                "peak_source": f"MEASURED_PEAKS.json hbm_gbs ({peak_kind})"},
+        "kernel_ms": t_kernel * 1e3,
+    }
+    line = {
+        "metric": metric, "value": value, "unit": "machine-steps/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16" if w <= 16 else "u32",
+        "data": "synthetic (generator G, SURVEY §8d; seed = rank)",
+        "config": {"workload": args.config, "desc": desc, "d_per_gpu": d, "w": w, "n": n,
+                   "ell": ell, "s": s, "tau_max": tau, "epoch": args.epoch,
+                   "machine_steps_per_gpu": machine_steps, "halted_frac": total_halted / (d * world),
+                   "l2": "flushed between steps (256 MB write, outside the events)",
+                   "parallelism": f"shard{world}" if world > 1 else "1 GPU"},
+        "programs_per_s": d * world / t_step,
+        "e2e": {"value": total_steps / t_e2e, "unit": "machine-steps/s",
+                "h2d_bytes_per_step": pipe.h2d_bytes, "d2h_bytes_per_step": pipe.d2h_bytes,
+                "ms_per_step": t_e2e * 1e3},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "clocks": clk,
+        "wall_s": wall,
+    }
+    if not args.no_cpu_baseline and world == 1:
+        cb = cpu_reference(args.config, 1, 0, args.cpu_sample)
+        line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,124 @@
+/*
+ * raspvisor_b200.h -- C ABI of the B200 word-RASP batch engine.
+ *
+ * Drop-in boundary for the reference's batch kernel.  The reference binds
+ * exactly one native entry point on this path,
+ *
+ *     _worker(iw, ac, M, u, y, status, steps, tau_h, g, W, q, rounds,
+ *             tau_max, wmask, n, ell, s)
+ *         /root/reference/pkg/src/raspvisor/hypervisor.py:128-164
+ *
+ * called once per host thread from run_batch (hypervisor.py:305-314) on
+ * C-contiguous SoA arrays it allocated itself.  rasp_run below replaces the
+ * W concurrent _worker calls with one device-side run over the whole batch:
+ * same arrays (device pointers, element width `word_bytes`), same in-place
+ * contract, same per-machine results, independent of `epoch` the way the
+ * reference is independent of (W, q) (hypervisor.py:1-9).
+ *
+ * Conventions: every pointer is a DEVICE pointer owned by the caller (torch
+ * tensors on the Python side); nothing here frees caller memory.  Every
+ * function returns 0 on success or a negative RASP_E* code; no exception
+ * crosses the ABI.  `stream` is a cudaStream_t passed as void*.  All work is
+ * enqueued on `stream`; nothing synchronises unless documented.
+ */
+#ifndef RASPVISOR_B200_H
+#define RASPVISOR_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RASP_ABI_VERSION 1
+
+/* error codes */
+#define RASP_OK 0
+#define RASP_EPARAM -1      /* bad machine params (hv:299-300 scalars / m:72-86) */
+#define RASP_ECAPACITY -2   /* batch or geometry beyond what the engine supports */
+#define RASP_ECUDA -3       /* a CUDA call failed; see rasp_last_cuda_error */
+#define RASP_EWORKSPACE -4  /* workspace too small */
+#define RASP_EDTYPE -5      /* word_bytes not in {1,2,4,8} or narrower than w */
+
+/* VM status codes: hypervisor.py:63-69 */
+#define RASP_RUNNING 0
+#define RASP_HALTED 1
+#define RASP_EXHAUSTED 2
+
+/* Machine geometry: the (wmask, n, ell, s) scalars of _worker
+ * (hypervisor.py:299-300), with w instead of wmask. */
+typedef struct rasp_params {
+    uint32_t w;    /* word width, 1..64 */
+    uint32_t n;    /* memory cells, >= 2 */
+    uint64_t ell;  /* input capacity, 1 <= ell < 2^w */
+    uint64_t s;    /* output capacity, 1 <= s < 2^w */
+} rasp_params;
+
+/* One batch of d machines in the reference's SoA layout (hypervisor.py:280-293):
+ * iw[d], ac[d], M[d][n], u[d][ell+1] (u[.][0] = read cursor),
+ * y[d][s+1] (y[.][0] = write count), all words of `word_bytes` bytes
+ * (1, 2, 4 or 8; at least ceil(w/8) rounded up to a power of two);
+ * status int8[d], steps int64[d], tau_h int64[d]. */
+typedef struct rasp_batch {
+    void *iw, *ac, *M, *u, *y;
+    int8_t *status;
+    int64_t *steps;
+    int64_t *tau_h;
+    uint64_t d;
+    uint32_t word_bytes;
+    uint32_t _pad;
+} rasp_batch;
+
+/* rasp_run flags */
+#define RASP_FRESH 1u   /* caller guarantees status == 0, steps == 0 on input
+                           (run_batch's fresh arrays, hv:291-293): skip reading them */
+
+/* Bytes of device workspace rasp_run needs for a batch of d machines. */
+size_t rasp_workspace_bytes(const rasp_params *p, uint64_t d);
+
+/* Run every RUNNING machine of `in` to a fixed point or tau_max total steps.
+ * Replaces the W calls of _worker (hypervisor.py:128-164 via :305-314).
+ *   in, out : may be the same batch (in-place, the reference's contract) or
+ *             two distinct batches of the same shape (out-of-place: `in` is
+ *             only read; every field of `out` is written).
+ *   Results per machine j, for any `epoch` >= 1:
+ *     HALTED    (status 1): tau_h = steps = least t with Phi^t(c) fixed, t <= tau_max
+ *     EXHAUSTED (status 2): steps = tau_max, tau_h unchanged (-1 from run_batch)
+ *     final config = Phi^steps(c);  machines entering with status != 0 are untouched.
+ *   epoch   : length of the first on-device epoch (the reference's q); later
+ *             epochs double it.  Performance knob only.
+ *   workspace: device buffer of at least rasp_workspace_bytes(p, d) bytes.
+ * Asynchronous on `stream` (may synchronise internally only when tau_max is
+ * too large for a fixed epoch schedule, to poll the live count). */
+int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out,
+             int64_t tau_max, int64_t epoch, uint32_t flags,
+             void *workspace, size_t workspace_bytes, void *stream);
+
+/* Bucketed halting-time histogram (hypervisor.py:326-352): out[0..99] exact
+ * tau_h, out[100] tau_h >= 100, out[101] EXHAUSTED count.  out: int64[102]
+ * device buffer, overwritten. */
+int rasp_histogram(const int8_t *status, const int64_t *tau_h, uint64_t d,
+                   int64_t *out, void *stream);
+
+/* Batch validation for run_batch (validate_config cursor ranges m:324-327 and
+ * the word-range check hv:285-290).  out: int64[8] device buffer, overwritten:
+ *   out[0..4] = count of words > 2^w-1 in iw, ac, M, u, y;
+ *   out[5] = count of u[.][0] > ell;  out[6] = count of y[.][0] > s;  out[7] = 0. */
+int rasp_validate(const rasp_params *p, const rasp_batch *b, int64_t *out, void *stream);
+
+/* Text for a RASP_E* code, and the last CUDA error string seen by this library. */
+const char *rasp_error_string(int code);
+const char *rasp_last_cuda_error(void);
+
+/* ABI version (RASP_ABI_VERSION) of the loaded library. */
+int rasp_abi_version(void);
+
+/* Cumulative number of kernels this library has launched (all threads). */
+unsigned long long rasp_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* RASPVISOR_B200_H */

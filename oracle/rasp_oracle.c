@@ -1,0 +1,185 @@
+/*
+ * rasp_oracle.c -- CPU restatement of the reference's batch transition map.
+ *
+ * TEST INFRASTRUCTURE ONLY.  This file is the parity checker and the CPU
+ * baseline ("port") for the B200 hot path.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load it.  The product
+ * path (paper_2604_12902_b200) never links or calls it.
+ *
+ * It restates, in C over the reference's own uint64 SoA layout:
+ *   oracle_advance  <- raspvisor/hypervisor.py:72-125   (_advance)
+ *   oracle_worker   <- raspvisor/hypervisor.py:128-164  (_worker)
+ *   oracle_run      <- raspvisor/hypervisor.py:295-314  (the W-thread
+ *                      striped dispatch inside run_batch)
+ * Semantics of one step follow raspvisor/machine.py:169-211
+ * (step_reference); the five-candidate fixedness test is hv:115-116.
+ *
+ * Parity pin: tests/test_oracle_golden.py checks every function here
+ * against fixtures produced by the reference itself
+ * (tests/golden/make_golden.py imports /root/reference/pkg/src).
+ */
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef uint64_t u64;
+typedef int64_t i64;
+
+enum { RUNNING = 0, HALTED = 1, EXHAUSTED = 2 };
+
+typedef struct {
+    u64 *iw, *ac, *M, *u, *y;     /* [d], [d], [d,n], [d,ell+1], [d,s+1] */
+    int8_t *status;               /* [d] */
+    i64 *steps, *tau_h;           /* [d] */
+    i64 d;
+    u64 wmask, n, ell, s;
+} oracle_state;
+
+/* hypervisor.py:72-125.  Returns 1 iff VM j is at a fixed point; otherwise
+ * applies one step when do_apply. */
+static int oracle_advance(const oracle_state *st, i64 j, int do_apply)
+{
+    const u64 n = st->n, wmask = st->wmask;
+    u64 *Mj = st->M + (size_t)j * n;
+    u64 *uj = st->u + (size_t)j * (st->ell + 1);
+    u64 *yj = st->y + (size_t)j * (st->s + 1);
+    const u64 i0 = st->iw[j];
+    const u64 a0 = st->ac[j];
+    const u64 o = Mj[i0 % n];                       /* hv:78 */
+    const u64 jw = Mj[((i0 + 1) & wmask) % n];      /* hv:79 */
+    const u64 jn = jw % n;                          /* hv:80 */
+    const u64 mj = Mj[jn];                          /* hv:81 */
+    const u64 u0 = uj[0], y0 = yj[0];
+
+    u64 ni = (i0 + 2) & wmask;                      /* hv:85 */
+    u64 na = a0, nm = mj, nu0 = u0, ny0 = y0;
+    int write_out = 0;
+    switch (o) {                                    /* hv:91-113 */
+    case 1: na = jw; break;                         /* LOD */
+    case 2: na = (a0 + mj) & wmask; break;          /* ADD */
+    case 3: na = (a0 * mj) & wmask; break;          /* MUL (wraps mod 2^64 first, as numpy) */
+    case 4: nm = a0; break;                         /* STO */
+    case 5: if (a0 != 0) ni = jw; break;            /* BNZ */
+    case 6:                                         /* RD */
+        if (u0 < st->ell) { nm = uj[u0 + 1]; nu0 = u0 + 1; }
+        else ni = i0;
+        break;
+    case 7:                                         /* PRI */
+        if (y0 < st->s) { ny0 = y0 + 1; write_out = 1; }
+        break;
+    default: ni = i0;
+    }
+    if (ni == i0 && na == a0 && nm == mj && nu0 == u0 && ny0 == y0)  /* hv:115 */
+        return 1;
+    if (do_apply) {                                 /* hv:117-124 */
+        st->iw[j] = ni;
+        st->ac[j] = na;
+        Mj[jn] = nm;
+        uj[0] = nu0;
+        if (write_out) yj[y0 + 1] = mj;
+        yj[0] = ny0;
+    }
+    return 0;
+}
+
+/* hypervisor.py:128-164: stripe {g + kW}, `rounds` sweeps of at most q
+ * steps per visit, budget probe, final classification sweep. */
+void oracle_worker(const oracle_state *st, i64 g, i64 W, i64 q, i64 rounds, i64 tau_max)
+{
+    const i64 d = st->d;
+    const i64 stripe = d > g ? (d - g + W - 1) / W : 0;
+    for (i64 r = 0; r < rounds; ++r) {
+        for (i64 k = 0; k < stripe; ++k) {
+            const i64 j = g + k * W;
+            if (st->status[j] != RUNNING) continue;
+            i64 applied = 0;
+            while (applied < q) {
+                if (st->steps[j] >= tau_max) {           /* hv:140-148 */
+                    if (oracle_advance(st, j, 0)) {
+                        st->status[j] = HALTED;
+                        st->tau_h[j] = st->steps[j];
+                    } else {
+                        st->status[j] = EXHAUSTED;
+                    }
+                    break;
+                }
+                if (oracle_advance(st, j, 1)) {          /* hv:149-152 */
+                    st->status[j] = HALTED;
+                    st->tau_h[j] = st->steps[j];
+                    break;
+                }
+                st->steps[j] += 1;                      /* hv:153-154 */
+                applied += 1;
+            }
+        }
+    }
+    for (i64 k = 0; k < stripe; ++k) {                   /* hv:157-164 */
+        const i64 j = g + k * W;
+        if (st->status[j] == RUNNING) {
+            if (oracle_advance(st, j, 0)) {
+                st->status[j] = HALTED;
+                st->tau_h[j] = st->steps[j];
+            } else {
+                st->status[j] = EXHAUSTED;
+            }
+        }
+    }
+}
+
+typedef struct {
+    const oracle_state *st;
+    i64 g, W, q, rounds, tau_max;
+} worker_arg;
+
+static void *worker_main(void *p)
+{
+    const worker_arg *a = (const worker_arg *)p;
+    oracle_worker(a->st, a->g, a->W, a->q, a->rounds, a->tau_max);
+    return NULL;
+}
+
+/* hypervisor.py:295-314: W = min(W, d) interleaved stripes, one thread each,
+ * epoch q, rounds = ceil(tau_max / q).  Returns 0 on success. */
+int oracle_run(u64 *iw, u64 *ac, u64 *M, u64 *u, u64 *y, int8_t *status,
+               i64 *steps, i64 *tau_h, i64 d, u64 wmask, u64 n, u64 ell, u64 s,
+               i64 tau_max, i64 q, i64 W)
+{
+    if (d <= 0) return 0;
+    if (q < 1 || tau_max < 0 || n < 2) return -1;
+    if (W < 1) W = 1;
+    if (W > d) W = d;
+    oracle_state st = {iw, ac, M, u, y, status, steps, tau_h, d, wmask, n, ell, s};
+    const i64 rounds = (tau_max + q - 1) / q;
+    if (W == 1) {
+        oracle_worker(&st, 0, 1, q, rounds, tau_max);
+        return 0;
+    }
+    pthread_t *th = (pthread_t *)malloc(sizeof(pthread_t) * (size_t)W);
+    worker_arg *args = (worker_arg *)malloc(sizeof(worker_arg) * (size_t)W);
+    if (!th || !args) { free(th); free(args); return -2; }
+    i64 started = 0;
+    for (i64 g = 0; g < W; ++g) {
+        args[g] = (worker_arg){&st, g, W, q, rounds, tau_max};
+        if (pthread_create(&th[g], NULL, worker_main, &args[g]) != 0) break;
+        ++started;
+    }
+    /* any stripe whose thread failed to start runs here, serially */
+    for (i64 g = started; g < W; ++g) worker_main(&args[g]);
+    for (i64 g = 0; g < started; ++g) pthread_join(th[g], NULL);
+    free(th);
+    free(args);
+    return 0;
+}
+
+/* Single step of one config held in caller arrays (machine.py:169-211).
+ * Writes the successor into the same arrays when not fixed; returns 1 iff
+ * the config is a fixed point.  Used by tests to cross-check KATs. */
+int oracle_step(u64 *i, u64 *a, u64 *M, u64 *u, u64 *y,
+                u64 wmask, u64 n, u64 ell, u64 s)
+{
+    int8_t status = 0;
+    i64 steps = 0, tau = -1;
+    oracle_state st = {i, a, M, u, y, &status, &steps, &tau, 1, wmask, n, ell, s};
+    return oracle_advance(&st, 0, 1);
+}

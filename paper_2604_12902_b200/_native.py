@@ -1,0 +1,89 @@
+"""ctypes binding of the C ABI in include/raspvisor_b200.h.
+
+The shared library is built in-tree (``__graft_entry__.build()`` or
+``python -m paper_2604_12902_b200.build``) into ``_lib/libraspvisor_b200.so``.
+There is no fallback: if the library is missing or cannot be loaded, every
+batch entry point raises NativeError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import NativeError
+
+LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
+LIB_PATH = os.path.join(LIB_DIR, "libraspvisor_b200.so")
+ABI_VERSION = 1
+
+RASP_FRESH = 1
+
+# symbols declared by include/raspvisor_b200.h
+EXPORTS = ("rasp_workspace_bytes", "rasp_run", "rasp_histogram", "rasp_validate",
+           "rasp_error_string", "rasp_last_cuda_error", "rasp_abi_version",
+           "rasp_launch_count")
+
+
+class RaspParams(ctypes.Structure):
+    _fields_ = [("w", ctypes.c_uint32), ("n", ctypes.c_uint32),
+                ("ell", ctypes.c_uint64), ("s", ctypes.c_uint64)]
+
+
+class RaspBatch(ctypes.Structure):
+    _fields_ = [("iw", ctypes.c_void_p), ("ac", ctypes.c_void_p), ("M", ctypes.c_void_p),
+                ("u", ctypes.c_void_p), ("y", ctypes.c_void_p),
+                ("status", ctypes.c_void_p), ("steps", ctypes.c_void_p),
+                ("tau_h", ctypes.c_void_p), ("d", ctypes.c_uint64),
+                ("word_bytes", ctypes.c_uint32), ("_pad", ctypes.c_uint32)]
+
+
+_lib = None
+
+
+def load():
+    """Load the engine library (once).  Raises NativeError when absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeError(
+            f"CUDA engine library not built: {LIB_PATH} is missing "
+            "(run __graft_entry__.build() or python -m paper_2604_12902_b200.build)")
+    try:
+        lib = ctypes.CDLL(LIB_PATH)
+    except OSError as e:
+        raise NativeError(f"cannot load {LIB_PATH}: {e}") from e
+    P, U64, I64, U32, SZ = (ctypes.c_void_p, ctypes.c_uint64, ctypes.c_int64,
+                            ctypes.c_uint32, ctypes.c_size_t)
+    pp = ctypes.POINTER(RaspParams)
+    pb = ctypes.POINTER(RaspBatch)
+    lib.rasp_workspace_bytes.argtypes = [pp, U64]
+    lib.rasp_workspace_bytes.restype = SZ
+    lib.rasp_run.argtypes = [pp, pb, pb, I64, I64, U32, P, SZ, P]
+    lib.rasp_run.restype = ctypes.c_int
+    lib.rasp_histogram.argtypes = [P, P, U64, P, P]
+    lib.rasp_histogram.restype = ctypes.c_int
+    lib.rasp_validate.argtypes = [pp, pb, P, P]
+    lib.rasp_validate.restype = ctypes.c_int
+    lib.rasp_error_string.argtypes = [ctypes.c_int]
+    lib.rasp_error_string.restype = ctypes.c_char_p
+    lib.rasp_last_cuda_error.argtypes = []
+    lib.rasp_last_cuda_error.restype = ctypes.c_char_p
+    lib.rasp_abi_version.argtypes = []
+    lib.rasp_abi_version.restype = ctypes.c_int
+    lib.rasp_launch_count.argtypes = []
+    lib.rasp_launch_count.restype = ctypes.c_ulonglong
+    if lib.rasp_abi_version() != ABI_VERSION:
+        raise NativeError(f"{LIB_PATH}: ABI version {lib.rasp_abi_version()} != {ABI_VERSION}")
+    _lib = lib
+    return lib
+
+
+def check(rc: int, what: str) -> None:
+    if rc != 0:
+        lib = load()
+        msg = lib.rasp_error_string(rc).decode()
+        if rc == -3:
+            msg += f" ({lib.rasp_last_cuda_error().decode()})"
+        raise NativeError(f"{what} failed: {msg} [code {rc}]")

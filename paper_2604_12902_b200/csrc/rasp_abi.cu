@@ -1,0 +1,326 @@
+// rasp_abi.cu -- extern "C" boundary of the B200 word-RASP engine
+// (declared in include/raspvisor_b200.h).  Host-side epoch scheduling,
+// template dispatch and launch configuration; the kernels are in
+// rasp_kernels.cuh.
+#include "rasp_kernels.cuh"
+#include "raspvisor_b200.h"
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+
+#include <atomic>
+
+namespace {
+
+thread_local char g_cuda_err[256] = "";
+std::atomic<unsigned long long> g_launches{0};
+
+int cuda_fail(cudaError_t e, const char *what)
+{
+    std::snprintf(g_cuda_err, sizeof g_cuda_err, "%s: %s", what, cudaGetErrorString(e));
+    return RASP_ECUDA;
+}
+
+#define RASP_CUDA(call)                                   \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+constexpr int kMaxEpochs = 1024;        // counter slots in the workspace
+constexpr int kPollAfter = 24;          // epochs after which the host polls the live count
+constexpr uint32_t kMaxK = 1u << 24;    // longest epoch, in steps
+constexpr int kWarpsPerBlockMax = 4;
+constexpr size_t kGlobalTileBudget = size_t(1) << 30;  // bytes of HBM tiles for huge n
+
+struct Device {
+    int id = -1, nsm = 0, smem_optin = 0;
+};
+
+int device_info(Device &dv)
+{
+    int id = 0;
+    RASP_CUDA(cudaGetDevice(&id));
+    static thread_local Device cache;
+    if (cache.id != id) {
+        Device d;
+        d.id = id;
+        RASP_CUDA(cudaDeviceGetAttribute(&d.nsm, cudaDevAttrMultiProcessorCount, id));
+        RASP_CUDA(cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, id));
+        cache = d;
+    }
+    dv = cache;
+    return RASP_OK;
+}
+
+size_t natural_bytes(uint32_t w) { return w <= 8 ? 1 : w <= 16 ? 2 : w <= 32 ? 4 : 8; }
+size_t cell_bytes(uint32_t w) { return w <= 32 ? 4 : 8; }
+size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+int check_params(const rasp_params *p)
+{
+    if (!p || p->w < 1 || p->w > 64 || p->n < 2) return RASP_EPARAM;
+    const uint64_t limit_m1 = p->w == 64 ? ~0ull : ((1ull << p->w) - 1);
+    if (p->ell < 1 || p->s < 1 || p->ell > limit_m1 || p->s > limit_m1) return RASP_EPARAM;
+    if (p->ell >= (1ull << 31) || p->s >= (1ull << 31)) return RASP_ECAPACITY;
+    return RASP_OK;
+}
+
+struct Plan {
+    bool smem = true;
+    int warps_per_block = 1;
+    int blocks = 1;
+    size_t tile_bytes = 0;
+    size_t dyn_smem = 0;
+    size_t gtile_bytes = 0;   // workspace bytes for HBM tiles (huge n only)
+};
+
+uint64_t tile_cells(const rasp_params *p) { return uint64_t(p->n) + p->ell + 1; }
+
+// Sizing that does not need the kernel handle (workspace size).
+void plan_shape(const rasp_params *p, const Device &dv, Plan &pl)
+{
+    pl.tile_bytes = tile_cells(p) * 32 * cell_bytes(p->w);
+    if (pl.tile_bytes <= size_t(dv.smem_optin)) {
+        pl.smem = true;
+        pl.warps_per_block = int(std::min<size_t>(kWarpsPerBlockMax, dv.smem_optin / pl.tile_bytes));
+        pl.dyn_smem = pl.tile_bytes * pl.warps_per_block;
+        pl.gtile_bytes = 0;
+    } else {
+        pl.smem = false;
+        pl.warps_per_block = 1;
+        pl.dyn_smem = 0;
+        const size_t warps = std::max<size_t>(
+            dv.nsm, std::min<size_t>(size_t(dv.nsm) * 16, kGlobalTileBudget / pl.tile_bytes));
+        pl.blocks = int(warps);
+        pl.gtile_bytes = warps * pl.tile_bytes;
+    }
+}
+
+struct Workspace {
+    uint32_t *lists[2];
+    uint32_t *counters;   // [kMaxEpochs][2]: tile counter, live count
+    void *gtiles;
+};
+
+size_t workspace_layout(const rasp_params *p, uint64_t d, const Plan &pl, void *base, Workspace *ws)
+{
+    size_t off = 0;
+    char *b = static_cast<char *>(base);
+    const size_t list_bytes = align256(sizeof(uint32_t) * std::max<uint64_t>(d, 1));
+    if (ws) ws->lists[0] = reinterpret_cast<uint32_t *>(b + off);
+    off += list_bytes;
+    if (ws) ws->lists[1] = reinterpret_cast<uint32_t *>(b + off);
+    off += list_bytes;
+    if (ws) ws->counters = reinterpret_cast<uint32_t *>(b + off);
+    off += align256(sizeof(uint32_t) * 2 * kMaxEpochs);
+    if (ws) ws->gtiles = pl.gtile_bytes ? b + off : nullptr;
+    off += align256(pl.gtile_bytes);
+    (void)p;
+    return off;
+}
+
+template <class S, class CT, bool POW2, bool GE2, bool SMEM>
+int launch_epochs(const rasp_params *p, const rasp::EpochArgs &base, Plan pl, const Device &dv,
+                  const Workspace &ws, uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
+{
+    auto kern = rasp::epoch_kernel<S, CT, POW2, GE2, SMEM>;
+    const int threads = 32 * pl.warps_per_block;
+    if (SMEM) {
+        RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.dyn_smem)));
+        int per_sm = 0;
+        RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, pl.dyn_smem));
+        if (per_sm < 1) return RASP_ECAPACITY;
+        pl.blocks = per_sm * dv.nsm;
+    }
+    const uint64_t tiles = (d + 31) / 32;
+    const uint64_t need_blocks = (tiles + pl.warps_per_block - 1) / pl.warps_per_block;
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(pl.blocks), need_blocks)));
+
+    RASP_CUDA(cudaMemsetAsync(ws.counters, 0, sizeof(uint32_t) * 2 * kMaxEpochs, st));
+    int64_t covered = 0;
+    uint64_t K = uint64_t(std::max<int64_t>(epoch, 1));
+    for (int e = 0;; ++e) {
+        if (e >= kMaxEpochs) return RASP_ECAPACITY;
+        if (e >= kPollAfter) {
+            uint32_t live = 0;
+            RASP_CUDA(cudaMemcpyAsync(&live, ws.counters + 2 * (e - 1) + 1, sizeof live,
+                                      cudaMemcpyDeviceToHost, st));
+            RASP_CUDA(cudaStreamSynchronize(st));
+            if (live == 0) break;
+        }
+        rasp::EpochArgs a = base;
+        const int64_t left = tau_max - covered;
+        a.K = uint32_t(std::min<uint64_t>(K, uint64_t(std::max<int64_t>(left, 0))));
+        a.first = e == 0;
+        a.list_in = e == 0 ? nullptr : ws.lists[(e - 1) & 1];
+        a.count_in_ptr = e == 0 ? nullptr : ws.counters + 2 * (e - 1) + 1;
+        a.count_in = e == 0 ? uint32_t(d) : 0;
+        a.list_out = ws.lists[e & 1];
+        a.tile_ctr = ws.counters + 2 * e;
+        a.count_out = ws.counters + 2 * e + 1;
+        kern<<<grid, threads, pl.dyn_smem, st>>>(a, static_cast<CT *>(ws.gtiles));
+        RASP_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        covered += a.K;
+        if (covered >= tau_max) break;
+        K = std::min<uint64_t>(K * 2, kMaxK);
+    }
+    return RASP_OK;
+}
+
+template <class S, class CT>
+int dispatch_flags(const rasp_params *p, const rasp::EpochArgs &a, const Plan &pl, const Device &dv,
+                   const Workspace &ws, uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
+{
+    const bool pow2 = (p->n & (p->n - 1)) == 0;
+    const bool ge2 = p->w >= 2;
+#define RASP_GO(P2, G2, SM) return launch_epochs<S, CT, P2, G2, SM>(p, a, pl, dv, ws, d, tau_max, epoch, st)
+    if (pl.smem) {
+        if (pow2) { if (ge2) RASP_GO(true, true, true); else RASP_GO(true, false, true); }
+        else { if (ge2) RASP_GO(false, true, true); else RASP_GO(false, false, true); }
+    } else {
+        if (pow2) { if (ge2) RASP_GO(true, true, false); else RASP_GO(true, false, false); }
+        else { if (ge2) RASP_GO(false, true, false); else RASP_GO(false, false, false); }
+    }
+#undef RASP_GO
+}
+
+rasp::Side side_of(const rasp_batch *b)
+{
+    rasp::Side s;
+    s.iw = b->iw; s.ac = b->ac; s.M = b->M; s.u = b->u; s.y = b->y;
+    s.status = b->status; s.steps = b->steps; s.tau_h = b->tau_h;
+    return s;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rasp_abi_version(void) { return RASP_ABI_VERSION; }
+
+unsigned long long rasp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+const char *rasp_error_string(int code)
+{
+    switch (code) {
+    case RASP_OK: return "ok";
+    case RASP_EPARAM: return "invalid machine parameters";
+    case RASP_ECAPACITY: return "batch or geometry exceeds engine capacity";
+    case RASP_ECUDA: return "CUDA error";
+    case RASP_EWORKSPACE: return "workspace too small";
+    case RASP_EDTYPE: return "word_bytes must be 1, 2, 4 or 8 and hold w bits";
+    default: return "unknown error";
+    }
+}
+
+const char *rasp_last_cuda_error(void) { return g_cuda_err; }
+
+size_t rasp_workspace_bytes(const rasp_params *p, uint64_t d)
+{
+    if (check_params(p) != RASP_OK) return 0;
+    Device dv;
+    if (device_info(dv) != RASP_OK) return 0;
+    Plan pl;
+    plan_shape(p, dv, pl);
+    return workspace_layout(p, d, pl, nullptr, nullptr);
+}
+
+int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, int64_t tau_max,
+             int64_t epoch, uint32_t flags, void *workspace, size_t workspace_bytes, void *stream)
+{
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!in || !out || tau_max < 0 || epoch < 1) return RASP_EPARAM;
+    if (in->d != out->d) return RASP_EPARAM;
+    const uint64_t d = in->d;
+    if (d == 0) return RASP_OK;
+    if (d > 0xffffffe0ull) return RASP_ECAPACITY;
+    const uint32_t wb = in->word_bytes;
+    if (wb != out->word_bytes || (wb != 1 && wb != 2 && wb != 4 && wb != 8) || wb < natural_bytes(p->w))
+        return RASP_EDTYPE;
+    Device dv;
+    rc = device_info(dv);
+    if (rc) return rc;
+    Plan pl;
+    plan_shape(p, dv, pl);
+    const size_t need = workspace_layout(p, d, pl, nullptr, nullptr);
+    if (!workspace || workspace_bytes < need) return RASP_EWORKSPACE;
+    Workspace ws;
+    workspace_layout(p, d, pl, workspace, &ws);
+
+    rasp::EpochArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.g.mask = p->w == 64 ? ~0ull : ((1ull << p->w) - 1);
+    a.g.n = p->n;
+    a.g.nm1 = p->n - 1;
+    a.g.jmask = a.g.mask & uint64_t(p->n - 1);
+    a.g.fm = ~0ull / p->n + 1;
+    a.g.ell = uint32_t(p->ell);
+    a.g.s = uint32_t(p->s);
+    a.in = side_of(in);
+    a.out = side_of(out);
+    a.tau_max = tau_max;
+    a.fresh = (flags & RASP_FRESH) ? 1 : 0;
+    a.inplace = (in->iw == out->iw) ? 1 : 0;
+    a.tile_cells = uint32_t(tile_cells(p));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+
+    if (p->w <= 32) {
+        switch (wb) {
+        case 1: return dispatch_flags<uint8_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+        case 2: return dispatch_flags<uint16_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+        case 4: return dispatch_flags<uint32_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+        default: return dispatch_flags<uint64_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+        }
+    }
+    return dispatch_flags<uint64_t, uint64_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+}
+
+int rasp_histogram(const int8_t *status, const int64_t *tau_h, uint64_t d, int64_t *out, void *stream)
+{
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!out) return RASP_EPARAM;
+    RASP_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t) * 102, st));
+    if (d == 0) return RASP_OK;
+    Device dv;
+    int rc = device_info(dv);
+    if (rc) return rc;
+    const uint64_t blocks = std::min<uint64_t>((d + 255) / 256, uint64_t(dv.nsm) * 8);
+    rasp::histogram_kernel<<<unsigned(blocks), 256, 0, st>>>(
+        status, tau_h, d, reinterpret_cast<unsigned long long *>(out));
+    RASP_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return RASP_OK;
+}
+
+int rasp_validate(const rasp_params *p, const rasp_batch *b, int64_t *out, void *stream)
+{
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!b || !out) return RASP_EPARAM;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    RASP_CUDA(cudaMemsetAsync(out, 0, sizeof(int64_t) * 8, st));
+    if (b->d == 0) return RASP_OK;
+    Device dv;
+    rc = device_info(dv);
+    if (rc) return rc;
+    const uint64_t mask = p->w == 64 ? ~0ull : ((1ull << p->w) - 1);
+    const unsigned blocks = unsigned(std::min<uint64_t>((b->d * p->n + 255) / 256, uint64_t(dv.nsm) * 8));
+    auto *o = reinterpret_cast<unsigned long long *>(out);
+    const rasp::Side s = side_of(b);
+    switch (b->word_bytes) {
+    case 1: rasp::validate_kernel<uint8_t><<<blocks, 256, 0, st>>>(s, b->d, p->n, p->ell + 1, p->s + 1, mask, p->ell, p->s, o); break;
+    case 2: rasp::validate_kernel<uint16_t><<<blocks, 256, 0, st>>>(s, b->d, p->n, p->ell + 1, p->s + 1, mask, p->ell, p->s, o); break;
+    case 4: rasp::validate_kernel<uint32_t><<<blocks, 256, 0, st>>>(s, b->d, p->n, p->ell + 1, p->s + 1, mask, p->ell, p->s, o); break;
+    case 8: rasp::validate_kernel<uint64_t><<<blocks, 256, 0, st>>>(s, b->d, p->n, p->ell + 1, p->s + 1, mask, p->ell, p->s, o); break;
+    default: return RASP_EDTYPE;
+    }
+    RASP_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return RASP_OK;
+}
+
+}  // extern "C"

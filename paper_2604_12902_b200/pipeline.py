@@ -1,0 +1,95 @@
+"""Host-buffer path: c0 in pinned host memory -> HBM -> run -> results back
+to pinned host memory, pipelined in chunks so the two PCIe directions and the
+engine overlap (copy-in of chunk c+1 and copy-out of chunk c-1 run under the
+compute of chunk c).
+
+This is the end-to-end path a caller with host arrays takes (the reference's
+run_batch consumes and returns host arrays, hypervisor.py:265-323).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from .engine import ALL_FIELDS, NUMPY_WORD, TORCH_WORD, WORD_FIELDS, DeviceBatch, Engine
+from .hypervisor import get_engine
+from .machine import MachineParams
+
+
+class HostPipeline:
+    def __init__(self, params: MachineParams, d: int, device=None, chunks: int = 8,
+                 engine: Engine | None = None, word_bytes: int | None = None):
+        self.params = params
+        self.d = d
+        self.device = torch.device(device) if device is not None else torch.device("cuda")
+        self.engine = engine or get_engine(params, self.device)
+        self.wb = word_bytes or params.dtype.itemsize
+        self.src = DeviceBatch.empty(d, params, self.device, self.wb, fresh=True)
+        self.dst = DeviceBatch.empty(d, params, self.device, self.wb, fresh=False)
+        self.chunks = max(1, min(chunks, (d + 4095) // 4096))
+        step = (d + self.chunks - 1) // self.chunks
+        self.bounds = [(a, min(d, a + step)) for a in range(0, d, step)] if d else []
+        wd = TORCH_WORD[self.wb]
+        shapes = {"iw": (d,), "ac": (d,), "M": (d, params.n), "u": (d, params.ell + 1),
+                  "y": (d, params.s + 1)}
+        self.host_out = {k: torch.empty(shapes[k], dtype=wd, pin_memory=True) for k in WORD_FIELDS}
+        self.host_out["status"] = torch.empty(d, dtype=torch.int8, pin_memory=True)
+        self.host_out["steps"] = torch.empty(d, dtype=torch.int64, pin_memory=True)
+        self.host_out["tau_h"] = torch.empty(d, dtype=torch.int64, pin_memory=True)
+        self.s_in = torch.cuda.Stream(self.device)
+        self.s_run = torch.cuda.Stream(self.device)
+        self.s_out = torch.cuda.Stream(self.device)
+        self.h2d_bytes = 0
+        self.d2h_bytes = sum(t.numel() * t.element_size() for t in self.host_out.values())
+        # one workspace per in-flight run (runs are serial on s_run, so one suffices)
+        self.engine.workspace(max((b - a for a, b in self.bounds), default=0))
+
+    def pinned_inputs(self, arrays: dict) -> dict:
+        """Copy host c0 arrays (numpy) into pinned tensors once."""
+        wd = TORCH_WORD[self.wb]
+        out = {}
+        for k in WORD_FIELDS:
+            a = np.ascontiguousarray(np.asarray(arrays[k]).astype(NUMPY_WORD[self.wb]))
+            t = torch.empty(a.shape, dtype=wd, pin_memory=True)
+            t.copy_(torch.from_numpy(a))
+            out[k] = t
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in out.values())
+        return out
+
+    @staticmethod
+    def _view(batch: DeviceBatch, a: int, b: int) -> DeviceBatch:
+        return DeviceBatch(batch.params, {k: getattr(batch, k)[a:b] for k in ALL_FIELDS},
+                           batch.word_bytes)
+
+    def run(self, pinned: dict, tau_max: int, epoch: int = 32) -> float:
+        """One end-to-end pass; returns device seconds (events on the caller's
+        stream bracketing every copy and every kernel)."""
+        main = torch.cuda.current_stream(self.device)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        for s in (self.s_in, self.s_run, self.s_out):
+            s.wait_event(e0)
+        for a, b in self.bounds:
+            with torch.cuda.stream(self.s_in):
+                for k in WORD_FIELDS:
+                    getattr(self.src, k)[a:b].copy_(pinned[k][a:b], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(self.s_in)
+            self.s_run.wait_event(ev_in)
+            self.engine.run(self._view(self.src, a, b), tau_max, epoch,
+                            out=self._view(self.dst, a, b), fresh=True, stream=self.s_run)
+            ev_run = torch.cuda.Event()
+            ev_run.record(self.s_run)
+            self.s_out.wait_event(ev_run)
+            with torch.cuda.stream(self.s_out):
+                for k in ALL_FIELDS:
+                    self.host_out[k][a:b].copy_(getattr(self.dst, k)[a:b], non_blocking=True)
+        main.wait_stream(self.s_out)
+        e1.record(main)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / 1e3
+
+    def results(self) -> dict:
+        return {k: v.numpy() for k, v in self.host_out.items()}

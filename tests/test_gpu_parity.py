@@ -1,0 +1,185 @@
+"""GPU parity: the CUDA engine (through the C ABI) against the reference's
+golden outputs (tests/golden, produced by raspvisor.run_batch) and the
+pinned CPU oracle.  Bit-exact on every field: final iw/ac/M/u/y, status,
+steps, tau_h."""
+
+import numpy as np
+import pytest
+
+from golden_io import FIELDS, RESULTS, load_all, load_family
+
+pytestmark = pytest.mark.gpu
+
+ALL = load_all()
+
+
+@pytest.fixture(scope="module")
+def pkg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.fail("GPU tests need a CUDA device")
+    import paper_2604_12902_b200 as P
+    from paper_2604_12902_b200 import hypervisor
+    return P, hypervisor
+
+
+def _params(P, g):
+    return P.MachineParams(w=g.w, n=g.n, ell=g.ell, s=g.s, mu=1)
+
+
+def _assert_same(res_arrays, g, tag=""):
+    for k in RESULTS:
+        got = np.asarray(res_arrays[k])
+        want = g.out[k]
+        if k in FIELDS:
+            got = got.astype(np.uint64)
+        np.testing.assert_array_equal(got, want, err_msg=f"{g} {tag} field {k}")
+
+
+def _slots_dict(sv):
+    return {k: getattr(sv, k) for k in RESULTS}
+
+
+@pytest.mark.parametrize("g", ALL, ids=repr)
+@pytest.mark.parametrize("epoch", [1, 7, 64])
+def test_engine_matches_reference_natural_width(pkg, g, epoch):
+    P, H = pkg
+    p = _params(P, g)
+    c0 = {k: g.c0[k].astype(p.dtype) for k in FIELDS}
+    res = H.run_arrays(c0, p, H.BatchConfig(tau_max=g.tau_max, epoch=epoch,
+                                            memory_budget_words=1 << 40))
+    _assert_same(_slots_dict(res.slots), g, f"epoch={epoch}")
+
+
+@pytest.mark.parametrize("g", [g for g in ALL if g.family in ("corpus", "hyp", "edge", "kat")],
+                         ids=repr)
+def test_engine_matches_reference_uint64_layout(pkg, g):
+    """The reference's own uint64 arrays, unconverted (word_bytes = 8)."""
+    P, H = pkg
+    p = _params(P, g)
+    res = H.run_arrays(dict(g.c0), p, H.BatchConfig(tau_max=g.tau_max, epoch=5,
+                                                    memory_budget_words=1 << 40))
+    assert res.slots.M.dtype == np.uint64
+    _assert_same(_slots_dict(res.slots), g, "u64")
+
+
+@pytest.mark.parametrize("g", load_family("corpus")[:7], ids=repr)
+def test_run_batch_tuple_api(pkg, g):
+    """The tuple interface returns the reference's SlotView/histogram."""
+    P, H = pkg
+    p = _params(P, g)
+    configs = [P.Config(int(g.c0["iw"][k]), int(g.c0["ac"][k]),
+                        tuple(int(v) for v in g.c0["M"][k]),
+                        tuple(int(v) for v in g.c0["u"][k]),
+                        tuple(int(v) for v in g.c0["y"][k])) for k in range(g.d)]
+    res = H.run_batch(configs, p, H.BatchConfig(tau_max=g.tau_max))
+    _assert_same(_slots_dict(res.slots), g, "tuples")
+    assert res.slots.iw.dtype == np.uint64
+    want = {}
+    for st, th in zip(g.out["status"], g.out["tau_h"]):
+        if st == 1:
+            want[int(th)] = want.get(int(th), 0) + 1
+    assert dict(res.histogram) == want
+    hist = H.collect_histogram(res.slots)
+    assert [hist[k] for k in H.HISTOGRAM_KEYS] == list(g.hist)
+
+
+@pytest.mark.parametrize("g", load_family("gen") + load_family("corpus")[:7], ids=repr)
+def test_out_of_place_and_device_histogram(pkg, g):
+    import torch
+    P, H = pkg
+    from paper_2604_12902_b200.engine import DeviceBatch
+    p = _params(P, g)
+    c0 = {k: g.c0[k].astype(p.dtype) for k in FIELDS}
+    src = DeviceBatch.from_arrays(c0, p)
+    before = {k: v.clone() for k, v in src.tensors().items()}
+    dst = DeviceBatch.empty(g.d, p, fresh=False)
+    eng = H.get_engine(p)
+    eng.run(src, g.tau_max, epoch=16, out=dst, fresh=True)
+    torch.cuda.synchronize()
+    for k, v in src.tensors().items():            # input untouched
+        assert torch.equal(v, before[k]), k
+    _assert_same(dst.to_numpy(), g, "out-of-place")
+    assert list(eng.histogram(dst).cpu().numpy()) == list(g.hist)
+
+
+def test_general_worker_contract(pkg):
+    """_worker semantics on mid-run inputs: nonzero initial steps, machines
+    already HALTED/EXHAUSTED are untouched (hv:136), tau_h left as given for
+    budget exhaustion.  Checked against the C oracle on the same arrays."""
+    P, H = pkg
+    from oracle import oracle
+    g = [x for x in load_family("corpus") if x.tau_max == 200][0]
+    p = _params(P, g)
+    rng = np.random.default_rng(7)
+    d = g.d
+    status = rng.choice(np.array([0, 0, 0, 1, 2], np.int8), d)
+    steps = rng.integers(0, 260, d).astype(np.int64)
+    tau_h = np.where(status == 1, steps, rng.integers(-1, 5, d)).astype(np.int64)
+    want = {k: np.ascontiguousarray(g.c0[k]).copy() for k in FIELDS}
+    want.update(status=status.copy(), steps=steps.copy(), tau_h=tau_h.copy())
+    oracle.oracle_run(want["iw"], want["ac"], want["M"], want["u"], want["y"], want["status"],
+                      want["steps"], want["tau_h"], g.w, g.n, g.ell, g.s, g.tau_max, 64, 1)
+    for epoch in (1, 64):
+        arrays = {k: g.c0[k].astype(p.dtype) for k in FIELDS}
+        arrays.update(status=status, steps=steps, tau_h=tau_h)
+        res = H.run_arrays(arrays, p, H.BatchConfig(tau_max=g.tau_max, epoch=epoch))
+        for k in RESULTS:
+            got = np.asarray(getattr(res.slots, k))
+            if k in FIELDS:
+                got = got.astype(np.uint64)
+            np.testing.assert_array_equal(got, want[k], err_msg=f"{k} epoch={epoch}")
+
+
+def test_bb_fixtures(pkg):
+    P, H = pkg
+    (g,) = load_family("bb")
+    p = _params(P, g)
+    res = H.run_arrays({k: g.c0[k].astype(p.dtype) for k in FIELDS}, p,
+                       H.BatchConfig(tau_max=10 ** 5))
+    assert list(res.slots.tau_h) == [1727, 1409, 1387]
+    assert list(res.slots.y[:, 0]) == [1, 1, 1] and list(res.slots.y[:, 1]) == [0, 0, 0]
+
+
+def test_validation_errors(pkg):
+    P, H = pkg
+    p = P.MachineParams(w=8, n=8, ell=2, s=2, mu=1)
+    good = P.init_config(P.Program((0, 0)), [], p)
+    bad = P.Config(i=0, a=0, M=(0, 300, 0, 0, 0, 0, 0, 0), u=good.u, y=good.y)
+    with pytest.raises(ValueError, match="2\\^w"):
+        H.run_batch([good, bad], p, H.BatchConfig(tau_max=1))
+    with pytest.raises(P.CapacityError, match="budget"):
+        H.run_batch([good] * 10, p, H.BatchConfig(tau_max=1, memory_budget_words=10))
+    with pytest.raises(ValueError):
+        H.run_batch([P.Config(0, 0, (0,) * 7, (0, 0, 0), (0, 0, 0))], p, H.BatchConfig(tau_max=1))
+    res = H.run_batch([], p, H.BatchConfig(tau_max=10))
+    assert len(res.slots) == 0 and res.histogram == {}
+
+
+def test_large_batch_against_oracle_sample(pkg):
+    """C2 shape at 2^20 machines: GPU vs oracle on a seeded 2^11 sample,
+    plus size-independent properties on the whole batch."""
+    P, H = pkg
+    from oracle import oracle
+    p = P.MachineParams(w=16, n=64, ell=8, s=8, mu=1)
+    d, tau = 1 << 20, 1024
+    c0 = P.synthetic_c0(d, p, seed=0)
+    res = H.run_arrays(c0, p, H.BatchConfig(tau_max=tau, epoch=32, memory_budget_words=1 << 40))
+    sv = res.slots
+    st, steps, th = sv.status, sv.steps, sv.tau_h
+    assert set(np.unique(st)) <= {1, 2}
+    assert (steps <= tau).all()
+    assert (th[st == 1] == steps[st == 1]).all()
+    assert (steps[st == 2] == tau).all() and (th[st == 2] == -1).all()
+    idx = np.sort(np.random.default_rng(1).choice(d, 2048, replace=False))
+    sample = {k: c0[k][idx] for k in FIELDS}
+    want = oracle.worker_arrays(sample, p.w, p.n, p.ell, p.s, tau)
+    for k in RESULTS:
+        got = np.asarray(getattr(sv, k))[idx]
+        if k in FIELDS:
+            got = got.astype(np.uint64)
+        np.testing.assert_array_equal(got, want[k], err_msg=k)
+    # epoch independence on the full batch
+    res2 = H.run_arrays(c0, p, H.BatchConfig(tau_max=tau, epoch=5, memory_budget_words=1 << 40))
+    for k in RESULTS:
+        assert np.array_equal(getattr(res2.slots, k), getattr(sv, k)), k
