@@ -76,7 +76,7 @@ struct Plan {
     size_t gtile_bytes = 0;   // workspace bytes for HBM tiles (huge n only)
 };
 
-uint64_t tile_cells(const rasp_params *p) { return uint64_t(p->n) + p->ell + 1; }
+uint64_t tile_cells(const rasp_params *p) { return uint64_t(p->n) + p->ell + 1 + p->s; }
 
 // Sizing that does not need the kernel handle (workspace size).
 void plan_shape(const rasp_params *p, const Device &dv, Plan &pl)
@@ -121,11 +121,11 @@ size_t workspace_layout(const rasp_params *p, uint64_t d, const Plan &pl, void *
     return off;
 }
 
-template <class S, class CT, bool POW2, bool GE2, bool SMEM>
-int launch_epochs(const rasp_params *p, const rasp::EpochArgs &base, Plan pl, const Device &dv,
-                  const Workspace &ws, uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
+template <class S, class CT, bool POW2, rasp::Arith AR, bool BUDGET, bool SMEM>
+int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const Workspace &ws,
+                  uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
 {
-    auto kern = rasp::epoch_kernel<S, CT, POW2, GE2, SMEM>;
+    auto kern = rasp::epoch_kernel<S, CT, POW2, AR, BUDGET, SMEM>;
     const int threads = 32 * pl.warps_per_block;
     if (SMEM) {
         RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.dyn_smem)));
@@ -153,6 +153,7 @@ int launch_epochs(const rasp_params *p, const rasp::EpochArgs &base, Plan pl, co
         rasp::EpochArgs a = base;
         const int64_t left = tau_max - covered;
         a.K = uint32_t(std::min<uint64_t>(K, uint64_t(std::max<int64_t>(left, 0))));
+        a.covered = covered;
         a.first = e == 0;
         a.list_in = e == 0 ? nullptr : ws.lists[(e - 1) & 1];
         a.count_in_ptr = e == 0 ? nullptr : ws.counters + 2 * (e - 1) + 1;
@@ -170,21 +171,35 @@ int launch_epochs(const rasp_params *p, const rasp::EpochArgs &base, Plan pl, co
     return RASP_OK;
 }
 
+template <class S, class CT, bool POW2, rasp::Arith AR>
+int dispatch_budget(const rasp::EpochArgs &a, const Plan &pl, const Device &dv, const Workspace &ws,
+                    uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
+{
+    if (a.fresh) return launch_epochs<S, CT, POW2, AR, false, true>(a, pl, dv, ws, d, tau_max, epoch, st);
+    return launch_epochs<S, CT, POW2, AR, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);
+}
+
 template <class S, class CT>
 int dispatch_flags(const rasp_params *p, const rasp::EpochArgs &a, const Plan &pl, const Device &dv,
                    const Workspace &ws, uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
 {
+    using rasp::Arith;
+    if (!pl.smem)   // huge n: tiles in HBM, generic arithmetic
+        return launch_epochs<S, CT, false, Arith::W1, true, false>(a, pl, dv, ws, d, tau_max, epoch, st);
     const bool pow2 = (p->n & (p->n - 1)) == 0;
-    const bool ge2 = p->w >= 2;
-#define RASP_GO(P2, G2, SM) return launch_epochs<S, CT, P2, G2, SM>(p, a, pl, dv, ws, d, tau_max, epoch, st)
-    if (pl.smem) {
-        if (pow2) { if (ge2) RASP_GO(true, true, true); else RASP_GO(true, false, true); }
-        else { if (ge2) RASP_GO(false, true, true); else RASP_GO(false, false, true); }
-    } else {
-        if (pow2) { if (ge2) RASP_GO(true, true, false); else RASP_GO(true, false, false); }
-        else { if (ge2) RASP_GO(false, true, false); else RASP_GO(false, false, false); }
+    const uint32_t bits = 8 * sizeof(CT);
+    if constexpr (sizeof(CT) == 4) {
+        if (p->w == 1) {
+            if (pow2) return dispatch_budget<S, CT, true, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
+            return dispatch_budget<S, CT, false, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
+        }
     }
-#undef RASP_GO
+    if (p->w == bits) {
+        if (pow2) return dispatch_budget<S, CT, true, Arith::FULL>(a, pl, dv, ws, d, tau_max, epoch, st);
+        return dispatch_budget<S, CT, false, Arith::FULL>(a, pl, dv, ws, d, tau_max, epoch, st);
+    }
+    if (pow2) return dispatch_budget<S, CT, true, Arith::NARROW>(a, pl, dv, ws, d, tau_max, epoch, st);
+    return dispatch_budget<S, CT, false, Arith::NARROW>(a, pl, dv, ws, d, tau_max, epoch, st);
 }
 
 rasp::Side side_of(const rasp_batch *b)
@@ -256,7 +271,7 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.g.mask = p->w == 64 ? ~0ull : ((1ull << p->w) - 1);
     a.g.n = p->n;
     a.g.nm1 = p->n - 1;
-    a.g.jmask = a.g.mask & uint64_t(p->n - 1);
+    a.g.jm = uint32_t(a.g.mask & uint64_t(p->n - 1));
     a.g.fm = ~0ull / p->n + 1;
     a.g.ell = uint32_t(p->ell);
     a.g.s = uint32_t(p->s);

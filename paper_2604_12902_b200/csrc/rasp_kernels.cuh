@@ -6,17 +6,19 @@
 // Execution model:
 //   * one machine per lane; i, a, u0, y0 and the step bookkeeping live in
 //     registers for a whole epoch of K steps;
-//   * each warp owns a private shared-memory tile: M (n rows) and the input
-//     tape u[1..ell] (ell+1 rows, one pad row), row-major with 32 lanes per
-//     row, so lane L's cell k sits at tile[k*32 + L] -- bank = lane for every
-//     data-dependent address, i.e. conflict-free random access;
-//   * the output tape y is write-only during a run and goes straight to HBM;
+//   * each warp owns a private shared-memory tile: M (n rows), the input
+//     tape u[1..ell] (ell+1 rows, one pad row) and s output rows, 32 lanes per row, so lane L's
+//     cell k sits at tile[k*32 + L] -- bank = lane for every data-dependent
+//     address, i.e. conflict-free random access;
+//   * the output tape y is write-only during a run: appended cells collect in
+//     tile rows and are flushed to HBM at the end of the epoch;
 //   * opcode dispatch is a predicated select over all candidates (no
-//     divergent branch on the opcode); the fixed-point test uses the
-//     equivalent short form of hv:115 for w >= 2;
+//     branch on the opcode); the fixed-point test uses the equivalent short
+//     form of hv:115 for w >= 2 and the full five-candidate
+//     equality for w = 1;
 //   * a warp leaves the epoch early when __any_sync says no lane is live;
 //   * epochs are separated by stream compaction: survivors are appended to
-//     the next live list (warp-aggregated atomics), halted machines retire.
+//     the next live list (warp-aggregated atomics), finished machines retire.
 #pragma once
 
 #include <cstdint>
@@ -26,15 +28,22 @@ namespace rasp {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int8_t kRunning = 0, kHalted = 1, kExhausted = 2;
+constexpr uint32_t kNoVerdict = 0xffffffffu;
+constexpr uint32_t kExhaustBit = 0x80000000u;
+
+// Word arithmetic regime: w == 1 (generic fixedness test), 2 <= w < bits(CT)
+// (masked), w == bits(CT) (native wrap-around, no masks).
+enum class Arith { W1, NARROW, FULL };
 
 struct Geo {
     uint64_t mask;    // 2^w - 1
     uint64_t fm;      // ceil(2^64 / n): Lemire fastmod magic (32-bit words, generic n)
-    uint64_t jmask;   // mask & (n - 1)   (power-of-two n)
     uint32_t n;
-    uint32_t nm1;     // n - 1            (power-of-two n)
+    uint32_t nm1;     // n - 1               (power-of-two n)
+    uint32_t jm;      // (2^w - 1) & (n - 1) (power-of-two n)
     uint32_t ell;
     uint32_t s;
+    uint32_t _pad;
 };
 
 struct Side {
@@ -53,13 +62,21 @@ struct EpochArgs {
     uint32_t *count_out;
     uint32_t *tile_ctr;
     int64_t tau_max;
+    int64_t covered;               // steps every fresh survivor has taken so far
     uint32_t count_in;
     uint32_t K;                    // applying steps in this epoch
     uint32_t first;                // read the batch from `in`
     uint32_t fresh;                // status=0, steps=0, tau_h=-1 on input
     uint32_t inplace;              // in == out
-    uint32_t tile_cells;           // n + ell + 1
+    uint32_t tile_cells;           // n + ell + 1 + s
 };
+
+template <class CT, Arith AR>
+__device__ __forceinline__ CT wrap(CT x, CT mask)
+{
+    if constexpr (AR == Arith::FULL) return x;
+    else return x & mask;
+}
 
 // x mod n for a word x.
 template <class CT, bool POW2>
@@ -75,22 +92,63 @@ __device__ __forceinline__ uint32_t modn(CT x, const Geo &g)
     }
 }
 
-// Per-lane row copy between a machine's HBM row (element type S, contiguous)
-// and its shared-memory column (element type CT, stride 32).
+// --- per-lane row movement between HBM (element S, contiguous) and the
+//     lane's shared-memory column (element CT, stride 32) --------------------
+
+template <class S, class CT>
+__device__ __forceinline__ void put16(CT *col, uint32_t k, const uint4 q)
+{
+    const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if constexpr (sizeof(S) == 1) {
+#pragma unroll
+            for (int b = 0; b < 4; ++b) col[(k + 4 * e + b) * 32] = static_cast<CT>((wv[e] >> (8 * b)) & 0xffu);
+        } else if constexpr (sizeof(S) == 2) {
+            col[(k + 2 * e) * 32] = static_cast<CT>(wv[e] & 0xffffu);
+            col[(k + 2 * e + 1) * 32] = static_cast<CT>(wv[e] >> 16);
+        } else if constexpr (sizeof(S) == 4) {
+            col[(k + e) * 32] = static_cast<CT>(wv[e]);
+        } else {
+            if (e & 1) continue;
+            col[(k + e / 2) * 32] = static_cast<CT>(static_cast<uint64_t>(wv[e]) |
+                                                    (static_cast<uint64_t>(wv[e + 1]) << 32));
+        }
+    }
+}
+
+template <class S, class CT>
+__device__ __forceinline__ uint4 get16(const CT *col, uint32_t k)
+{
+    uint32_t wv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        if constexpr (sizeof(S) == 1) {
+            uint32_t x = 0;
+#pragma unroll
+            for (int b = 0; b < 4; ++b) x |= (static_cast<uint32_t>(col[(k + 4 * e + b) * 32]) & 0xffu) << (8 * b);
+            wv[e] = x;
+        } else if constexpr (sizeof(S) == 2) {
+            wv[e] = (static_cast<uint32_t>(col[(k + 2 * e) * 32]) & 0xffffu) |
+                    (static_cast<uint32_t>(col[(k + 2 * e + 1) * 32]) << 16);
+        } else if constexpr (sizeof(S) == 4) {
+            wv[e] = static_cast<uint32_t>(col[(k + e) * 32]);
+        } else {
+            const uint64_t v = static_cast<uint64_t>(col[(k + e / 2) * 32]);
+            wv[e] = (e & 1) ? static_cast<uint32_t>(v >> 32) : static_cast<uint32_t>(v);
+        }
+    }
+    return make_uint4(wv[0], wv[1], wv[2], wv[3]);
+}
+
 template <class S, class CT>
 __device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t ncells, CT *col)
 {
     constexpr uint32_t PER = 16 / sizeof(S);
     uint32_t k = 0;
-    if (((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+    if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
         const uint4 *v = reinterpret_cast<const uint4 *>(row);
-        for (; k + PER <= ncells; k += PER) {
-            const uint4 q = v[k / PER];
-            S e[PER];
-            memcpy(e, &q, 16);
-#pragma unroll
-            for (uint32_t p = 0; p < PER; ++p) col[(k + p) * 32] = static_cast<CT>(e[p]);
-        }
+        for (; k + PER <= ncells; k += PER) put16<S, CT>(col, k, v[k / PER]);
     }
     for (; k < ncells; ++k) col[k * 32] = static_cast<CT>(row[k]);
 }
@@ -100,16 +158,9 @@ __device__ __forceinline__ void store_row(S *__restrict__ row, uint32_t ncells, 
 {
     constexpr uint32_t PER = 16 / sizeof(S);
     uint32_t k = 0;
-    if (((reinterpret_cast<uintptr_t>(row) & 15) == 0)) {
+    if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
         uint4 *v = reinterpret_cast<uint4 *>(row);
-        for (; k + PER <= ncells; k += PER) {
-            S e[PER];
-#pragma unroll
-            for (uint32_t p = 0; p < PER; ++p) e[p] = static_cast<S>(col[(k + p) * 32]);
-            uint4 q;
-            memcpy(&q, e, 16);
-            v[k / PER] = q;
-        }
+        for (; k + PER <= ncells; k += PER) v[k / PER] = get16<S, CT>(col, k);
     }
     for (; k < ncells; ++k) row[k] = static_cast<S>(col[k * 32]);
 }
@@ -120,107 +171,172 @@ __device__ __forceinline__ void copy_cells(S *__restrict__ dst, const S *__restr
     for (uint64_t k = 0; k < n; ++k) dst[k] = src[k];
 }
 
-// One machine held by one lane.  `sM`/`sU` point at the lane's column.
-template <class S, class CT, bool POW2, bool GE2>
-struct Lane {
+// --- one machine per lane -------------------------------------------------------
+//
+// Tile layout per warp (byte offsets from the warp's tile base `tb`, cells of
+// type CT, 32 lanes per row, lane L at +L*sizeof(CT)):
+//   rows [0, n)            M
+//   rows [n, n+ell+1)      u[1..ell] + one pad row (u[u0+1] is read every step)
+//   rows [n+ell+1, +s)     y[1..s] written during this epoch (flushed at its end)
+// Cursors are kept as byte offsets (ua = U + u0*row, ya = Y + y0*row) so the
+// hot loop does no address arithmetic for them.
+
+template <class CT>
+struct LaneState {
     CT i, a;
-    uint32_t u0, y0;
-    uint32_t rem;      // remaining budget at epoch start (clamped)
-    uint32_t tfin;     // step index of the verdict within this epoch
-    bool active, halted, dirty;
-
-    // Evaluate the step at local time t; classify or (if apply) commit it.
-    // The five-candidate equality of hv:115 decides fixedness; for w >= 2
-    // it reduces to: o not in 1..7, RD at capacity, or BNZ taken to itself.
-    __device__ __forceinline__ void step(CT *sM, const CT *sU, S *yrow, const Geo &g,
-                                         uint32_t t, bool apply)
-    {
-        const CT mask = static_cast<CT>(g.mask);
-        const uint32_t ia = modn<CT, POW2>(i, g);
-        uint32_t ib;
-        if constexpr (POW2) ib = static_cast<uint32_t>((i + 1) & static_cast<CT>(g.jmask));
-        else ib = modn<CT, POW2>((i + 1) & mask, g);
-        const CT o = sM[ia * 32];
-        const CT jw = sM[ib * 32];
-        const uint32_t jn = modn<CT, POW2>(jw, g);
-        const CT mj = sM[jn * 32];
-        const CT ud = sU[u0 * 32];
-
-        const bool is_rd = (o == 6);
-        const bool rd_ok = is_rd & (u0 < g.ell);
-        const bool pri_ok = (o == 7) & (y0 < g.s);
-        const bool taken = (o == 5) & (a != 0);
-        const bool is_sto = (o == 4);
-        const CT i2 = (i + 2) & mask;
-        CT na = a;
-        na = (o == 3) ? static_cast<CT>((a * mj) & mask) : na;
-        na = (o == 2) ? static_cast<CT>((a + mj) & mask) : na;
-        na = (o == 1) ? jw : na;
-        const CT nm = is_sto ? a : ud;
-        const bool wr = is_sto | rd_ok;
-        bool fixed;
-        CT ni;
-        if constexpr (GE2) {
-            fixed = (static_cast<CT>(o - 1) > 6) | (is_rd & !rd_ok) | (taken & (jw == i));
-            ni = taken ? jw : i2;
-        } else {
-            const bool adv = (static_cast<CT>(o - 1) < 4) | ((o == 5) & (a == 0)) | rd_ok | (o == 7);
-            ni = taken ? jw : (adv ? i2 : i);
-            const CT nmf = wr ? nm : mj;
-            fixed = (ni == i) & (na == a) & (nmf == mj) & !rd_ok & !pri_ok;
-        }
-        if (active) {
-            if (fixed) {
-                halted = true;
-                tfin = t;
-                active = false;
-            } else if (t == rem) {
-                tfin = t;
-                active = false;
-            } else if (apply) {
-                i = ni;
-                a = na;
-                if (wr) {
-                    sM[jn * 32] = nm;
-                    dirty = true;
-                }
-                u0 += rd_ok ? 1u : 0u;
-                if (pri_ok) {
-                    yrow[y0] = static_cast<S>(mj);
-                    ++y0;
-                }
-            }
-        }
-    }
+    uint32_t ua, ya;  // addresses of u[u0+1] and y[y0+1] in the tile
+    uint32_t rem;     // remaining budget at epoch start (clamped)
+    uint32_t tfin;    // verdict time within the epoch (| kExhaustBit), or kNoVerdict
+    bool active;
 };
 
-template <class S, class CT, bool POW2, bool GE2, bool SMEM>
+// Cell access.  SMEM kernels address the warp tile with 32-bit shared-window
+// addresses (one LDS/STS with a register address per access); the huge-n
+// fallback uses byte offsets from the warp's HBM tile `base`.
+template <class CT, bool SMEM>
+__device__ __forceinline__ CT ld_cell(char *base, uint32_t a)
+{
+    if constexpr (SMEM) {
+        if constexpr (sizeof(CT) == 4) {
+            uint32_t v;
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+            return v;
+        } else {
+            unsigned long long v;
+            asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
+            return static_cast<CT>(v);
+        }
+    } else {
+        return *reinterpret_cast<const volatile CT *>(base + a);
+    }
+}
+
+template <class CT, bool SMEM>
+__device__ __forceinline__ void st_cell(char *base, uint32_t a, CT v)
+{
+    if constexpr (SMEM) {
+        if constexpr (sizeof(CT) == 4) {
+            asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(static_cast<uint32_t>(v)) : "memory");
+        } else {
+            asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(static_cast<unsigned long long>(v)) : "memory");
+        }
+    } else {
+        *reinterpret_cast<volatile CT *>(base + a) = v;
+    }
+}
+
+// Evaluate the step at local time t and, when allowed, commit it.
+// Fixedness (hv:115): the next configuration equals the current one.  For
+// w >= 2, (i+2) mod 2^w != i, so every advancing case moves i and the test
+// reduces to: opcode not in 1..7, RD with the cursor at capacity, or BNZ
+// taken to its own address.  BUDGET: check t == rem inside the loop (runs
+// whose machines did not all start at the same step count); the final,
+// non-applying evaluation at t == K always checks it.
+template <class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
+__device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
+                                          uint32_t yend, const Geo &g, uint32_t t, bool can_apply)
+{
+    constexpr uint32_t SH = sizeof(CT) == 4 ? 7 : 8;   // log2(row bytes)
+    constexpr uint32_t ROW = 1u << SH;
+    const CT mask = static_cast<CT>(g.mask);
+    uint32_t ia, ib;
+    if constexpr (POW2) {
+        ia = static_cast<uint32_t>(L.i) & g.nm1;
+        ib = static_cast<uint32_t>(L.i + 1) & g.jm;
+    } else {
+        ia = modn<CT, POW2>(L.i, g);
+        ib = modn<CT, POW2>(wrap<CT, AR>(L.i + 1, mask), g);
+    }
+    const CT o = ld_cell<CT, SMEM>(base, (ia << SH) + lm);
+    const CT jw = ld_cell<CT, SMEM>(base, (ib << SH) + lm);
+    const uint32_t jo = (modn<CT, POW2>(jw, g) << SH) + lm;
+    const CT mj = ld_cell<CT, SMEM>(base, jo);
+    const CT ud = ld_cell<CT, SMEM>(base, L.ua);
+    const CT a0 = L.a;
+
+    const bool rd = (o == 6) & (L.ua < uend);
+    const bool taken = (o == 5) & (a0 != 0);
+    const bool pri = (o == 7) & (L.ya < yend);
+    const CT i2 = wrap<CT, AR>(L.i + 2, mask);
+    CT na = (o == 1) ? jw : a0;
+    na = (o == 2) ? static_cast<CT>(a0 + mj) : na;
+    na = (o == 3) ? static_cast<CT>(a0 * mj) : na;
+    na = wrap<CT, AR>(na, mask);
+    const CT nm = (o == 4) ? a0 : ud;
+    bool fixed;
+    CT ni;
+    if constexpr (AR != Arith::W1) {
+        fixed = (o == 0) | (o > 7) | ((o == 6) & !rd) | (taken & (jw == L.i));
+        ni = taken ? jw : i2;
+    } else {
+        const bool adv = (static_cast<CT>(o - 1) < 4) | ((o == 5) & (a0 == 0)) | rd | (o == 7);
+        ni = taken ? jw : (adv ? i2 : L.i);
+        const CT nmf = ((o == 4) | rd) ? nm : mj;
+        fixed = (ni == L.i) & (na == a0) & (nmf == mj) & !rd & !pri;
+    }
+    if (BUDGET || !can_apply) {
+        const bool fin = L.active & (fixed | (t == L.rem));
+        if (fin) L.tfin = fixed ? t : (t | kExhaustBit);
+        L.active = L.active & !fin;
+    } else {
+        if (L.active & fixed) L.tfin = t;
+        L.active = L.active & !fixed;
+    }
+    const bool app = L.active & can_apply;
+    if (app) {
+        L.i = ni;
+        L.a = na;
+    }
+    if (app & ((o == 4) | rd)) st_cell<CT, SMEM>(base, jo, nm);
+    const bool wy = app & pri;
+    if (wy) st_cell<CT, SMEM>(base, L.ya, mj);
+    if (app & rd) L.ua += ROW;
+    if (wy) L.ya += ROW;
+}
+
+template <class S, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
 __global__ void __launch_bounds__(128)
 epoch_kernel(const EpochArgs A, CT *gtiles)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr uint32_t ROW = 32 * sizeof(CT);
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
     const Geo g = A.g;
     const uint32_t n = g.n;
     const uint64_t ucols = static_cast<uint64_t>(g.ell) + 1;
     const uint64_t ycols = static_cast<uint64_t>(g.s) + 1;
+    const uint32_t tile_bytes = A.tile_cells * ROW;
 
-    CT *tile;
+    char *tb;      // SMEM: the dynamic shared window; else the warp's HBM tile
+    uint32_t lm;   // address of this lane's column in row 0
     if constexpr (SMEM) {
-        tile = reinterpret_cast<CT *>(smem_raw) + static_cast<size_t>(wib) * A.tile_cells * 32;
+        tb = reinterpret_cast<char *>(smem_raw);
+        lm = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes +
+             lane * static_cast<uint32_t>(sizeof(CT));
     } else {
-        tile = gtiles + (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + wib) *
-                            static_cast<size_t>(A.tile_cells) * 32;
+        tb = reinterpret_cast<char *>(gtiles) +
+             (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * static_cast<size_t>(tile_bytes);
+        lm = lane * static_cast<uint32_t>(sizeof(CT));
     }
-    CT *sM = tile + lane;
-    CT *sU = sM + static_cast<size_t>(n) * 32;
+    const uint32_t U = n * ROW + lm;                       // u[1] of this lane
+    const uint32_t Y = (n + g.ell + 1) * ROW + lm;         // y[1] of this lane (epoch scratch)
+    const uint32_t uend = U + g.ell * ROW;
+    const uint32_t yend = Y + g.s * ROW;
+    // generic pointers to this lane's columns, for the (cold) row copies
+    char *gb = SMEM ? reinterpret_cast<char *>(smem_raw) -
+                          static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw))
+                    : tb;
+    CT *colM = reinterpret_cast<CT *>(gb + lm);
+    CT *colU = reinterpret_cast<CT *>(gb + U);
+    CT *colY = reinterpret_cast<CT *>(gb + Y);
 
     const uint32_t count = A.count_in_ptr ? *A.count_in_ptr : A.count_in;
     const uint32_t ntiles = (count + 31) / 32;
     const Side &src = A.first ? A.in : A.out;
     const Side &dst = A.out;
     const bool copy_side = A.first && !A.inplace;
+    const bool fresh = A.fresh != 0;
 
     for (;;) {
         uint32_t tix = 0;
@@ -231,22 +347,20 @@ epoch_kernel(const EpochArgs A, CT *gtiles)
         const bool valid = j < count;
         const uint64_t id = valid ? (A.list_in ? A.list_in[j] : j) : 0;
 
-        Lane<S, CT, POW2, GE2> L;
-        L.i = 0; L.a = 0; L.u0 = 0; L.y0 = 0; L.tfin = 0;
-        L.halted = false; L.dirty = false;
+        LaneState<CT> L;
+        L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tfin = kNoVerdict;
         bool running = valid;
-        int64_t steps0 = 0;
-        if (valid) {
+        int64_t steps0 = fresh ? A.covered : 0;
+        if (valid && !fresh) {
             if (A.first) {
-                if (!A.fresh) {
-                    const int8_t st = A.in.status[id];
-                    if (st != kRunning) running = false;
-                    else steps0 = A.in.steps[id];
-                    if (copy_side) {
-                        dst.status[id] = st;
-                        dst.steps[id] = A.in.steps[id];
-                        dst.tau_h[id] = A.in.tau_h[id];
-                    }
+                const int8_t st = A.in.status[id];
+                const int64_t s0 = A.in.steps[id];
+                if (st != kRunning) running = false;
+                steps0 = s0;
+                if (copy_side) {
+                    dst.status[id] = st;
+                    dst.steps[id] = s0;
+                    dst.tau_h[id] = A.in.tau_h[id];
                 }
             } else {
                 steps0 = dst.steps[id];
@@ -263,13 +377,15 @@ epoch_kernel(const EpochArgs A, CT *gtiles)
             copy_cells(static_cast<S *>(dst.u) + id * ucols, srcU, ucols);
             copy_cells(static_cast<S *>(dst.y) + id * ycols, srcY, ycols);
         }
+        uint32_t y0_start = 0;
         if (running) {
             L.i = static_cast<CT>(static_cast<const S *>(src.iw)[id]);
             L.a = static_cast<CT>(static_cast<const S *>(src.ac)[id]);
-            L.u0 = static_cast<uint32_t>(srcU[0]);
-            L.y0 = static_cast<uint32_t>(srcY[0]);
-            load_row<S, CT>(srcM, n, sM);
-            load_row<S, CT>(srcU + 1, g.ell, sU);
+            L.ua = U + static_cast<uint32_t>(srcU[0]) * ROW;
+            y0_start = static_cast<uint32_t>(srcY[0]);
+            L.ya = Y + y0_start * ROW;
+            load_row<S, CT>(srcM, n, colM);
+            load_row<S, CT>(srcU + 1, g.ell, colU);
             if (copy_side) {
                 copy_cells(static_cast<S *>(dst.u) + id * ucols + 1, srcU + 1, g.ell);
                 copy_cells(static_cast<S *>(dst.y) + id * ycols + 1, srcY + 1, g.s);
@@ -279,39 +395,47 @@ epoch_kernel(const EpochArgs A, CT *gtiles)
                                                      : static_cast<uint64_t>(A.tau_max - steps0);
         L.rem = rem64 > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(rem64);
         L.active = running;
-        S *yrow = static_cast<S *>(dst.y) + id * ycols + 1;
+        asm volatile("" ::: "memory");   // column fills above are visible to the asm loads below
 
         const uint32_t K = A.K;
         uint32_t t = 0;
-        for (; t < K; ++t) {
-            if (!__any_sync(kFull, L.active)) break;
-            L.step(sM, sU, yrow, g, t, true);
+        bool live = __any_sync(kFull, L.active);
+        for (; live && t + 2 <= K; t += 2) {
+            rasp_step<CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t, true);
+            rasp_step<CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t + 1, true);
+            live = __any_sync(kFull, L.active);
         }
-        if (t == K && __any_sync(kFull, L.active)) L.step(sM, sU, yrow, g, t, false);
+        if (live && t < K) {
+            rasp_step<CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t, true);
+            ++t;
+            live = __any_sync(kFull, L.active);
+        }
+        if (live) rasp_step<CT, POW2, AR, true, SMEM>(L, tb, lm, uend, yend, g, K, false);
 
         bool survivor = false;
         if (running) {
+            const uint32_t u0 = (L.ua - U) / ROW;
+            const uint32_t y0 = (L.ya - Y) / ROW;
+            S *dY = static_cast<S *>(dst.y) + id * ycols;
             static_cast<S *>(dst.iw)[id] = static_cast<S>(L.i);
             static_cast<S *>(dst.ac)[id] = static_cast<S>(L.a);
-            static_cast<S *>(dst.u)[id * ucols] = static_cast<S>(L.u0);
-            static_cast<S *>(dst.y)[id * ycols] = static_cast<S>(L.y0);
-            if (L.dirty || copy_side) store_row<S, CT>(static_cast<S *>(dst.M) + id * n, n, sM);
-            if (L.halted) {
-                const int64_t tau = steps0 + L.tfin;
-                dst.status[id] = kHalted;
-                dst.steps[id] = tau;
-                dst.tau_h[id] = tau;
-            } else if (!L.active) {
-                dst.status[id] = kExhausted;
-                dst.steps[id] = steps0 + L.tfin;
-                if (A.fresh && copy_side) dst.tau_h[id] = -1;
+            static_cast<S *>(dst.u)[id * ucols] = static_cast<S>(u0);
+            dY[0] = static_cast<S>(y0);
+            for (uint32_t k = y0_start; k < y0; ++k) dY[k + 1] = static_cast<S>(colY[k * 32]);
+            store_row<S, CT>(static_cast<S *>(dst.M) + id * n, n, colM);
+            if (L.tfin != kNoVerdict) {
+                const int64_t tend = steps0 + (L.tfin & ~kExhaustBit);
+                dst.steps[id] = tend;
+                if (L.tfin & kExhaustBit) {
+                    dst.status[id] = kExhausted;
+                    if (fresh) dst.tau_h[id] = -1;
+                } else {
+                    dst.status[id] = kHalted;
+                    dst.tau_h[id] = tend;
+                }
             } else {
                 survivor = true;
-                dst.steps[id] = steps0 + K;
-                if (A.fresh && copy_side) {
-                    dst.status[id] = kRunning;
-                    dst.tau_h[id] = -1;
-                }
+                if (!fresh) dst.steps[id] = steps0 + K;
             }
         }
         const unsigned sv = __ballot_sync(kFull, survivor);
