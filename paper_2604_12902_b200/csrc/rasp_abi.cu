@@ -55,7 +55,7 @@ int device_info(Device &dv)
 }
 
 size_t natural_bytes(uint32_t w) { return w <= 8 ? 1 : w <= 16 ? 2 : w <= 32 ? 4 : 8; }
-size_t cell_bytes(uint32_t w) { return w <= 32 ? 4 : 8; }
+size_t cell_bytes(uint32_t w) { return w <= 16 ? 2 : w <= 32 ? 4 : 8; }   // tile cell SC
 size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 
 int check_params(const rasp_params *p)
@@ -76,12 +76,12 @@ struct Plan {
     size_t gtile_bytes = 0;   // workspace bytes for HBM tiles (huge n only)
 };
 
-uint64_t tile_cells(const rasp_params *p) { return uint64_t(p->n) + p->ell + 1 + p->s; }
+uint64_t tile_rows(const rasp_params *p) { return uint64_t(p->n) + p->ell + 1 + p->s; }
 
 // Sizing that does not need the kernel handle (workspace size).
 void plan_shape(const rasp_params *p, const Device &dv, Plan &pl)
 {
-    pl.tile_bytes = tile_cells(p) * 32 * cell_bytes(p->w);
+    pl.tile_bytes = tile_rows(p) * 32 * cell_bytes(p->w);
     if (pl.tile_bytes <= size_t(dv.smem_optin)) {
         pl.smem = true;
         pl.warps_per_block = int(std::min<size_t>(kWarpsPerBlockMax, dv.smem_optin / pl.tile_bytes));
@@ -121,11 +121,11 @@ size_t workspace_layout(const rasp_params *p, uint64_t d, const Plan &pl, void *
     return off;
 }
 
-template <class S, class CT, bool POW2, rasp::Arith AR, bool BUDGET, bool SMEM>
+template <class S, class SC, class CT, bool POW2, rasp::Arith AR, bool BUDGET, bool SMEM>
 int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const Workspace &ws,
                   uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
 {
-    auto kern = rasp::epoch_kernel<S, CT, POW2, AR, BUDGET, SMEM>;
+    auto kern = rasp::epoch_kernel<S, SC, CT, POW2, AR, BUDGET, SMEM>;
     const int threads = 32 * pl.warps_per_block;
     if (SMEM) {
         RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.dyn_smem)));
@@ -161,7 +161,7 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
         a.list_out = ws.lists[e & 1];
         a.tile_ctr = ws.counters + 2 * e;
         a.count_out = ws.counters + 2 * e + 1;
-        kern<<<grid, threads, pl.dyn_smem, st>>>(a, static_cast<CT *>(ws.gtiles));
+        kern<<<grid, threads, pl.dyn_smem, st>>>(a, static_cast<SC *>(ws.gtiles));
         RASP_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
         covered += a.K;
@@ -171,35 +171,36 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
     return RASP_OK;
 }
 
-template <class S, class CT, bool POW2, rasp::Arith AR>
+template <class S, class SC, class CT, bool POW2, rasp::Arith AR>
 int dispatch_budget(const rasp::EpochArgs &a, const Plan &pl, const Device &dv, const Workspace &ws,
                     uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
 {
-    if (a.fresh) return launch_epochs<S, CT, POW2, AR, false, true>(a, pl, dv, ws, d, tau_max, epoch, st);
-    return launch_epochs<S, CT, POW2, AR, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);
+    if (a.fresh) return launch_epochs<S, SC, CT, POW2, AR, false, true>(a, pl, dv, ws, d, tau_max, epoch, st);
+    return launch_epochs<S, SC, CT, POW2, AR, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);
 }
 
-template <class S, class CT>
+// S: HBM word type, SC: tile cell type, CT: arithmetic type.
+template <class S, class SC, class CT>
 int dispatch_flags(const rasp_params *p, const rasp::EpochArgs &a, const Plan &pl, const Device &dv,
                    const Workspace &ws, uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
 {
     using rasp::Arith;
     if (!pl.smem)   // huge n: tiles in HBM, generic arithmetic
-        return launch_epochs<S, CT, false, Arith::W1, true, false>(a, pl, dv, ws, d, tau_max, epoch, st);
+        return launch_epochs<S, SC, CT, false, Arith::W1, true, false>(a, pl, dv, ws, d, tau_max, epoch, st);
     const bool pow2 = (p->n & (p->n - 1)) == 0;
-    const uint32_t bits = 8 * sizeof(CT);
-    if constexpr (sizeof(CT) == 4) {
+    if constexpr (sizeof(SC) == 2) {
         if (p->w == 1) {
-            if (pow2) return dispatch_budget<S, CT, true, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
-            return dispatch_budget<S, CT, false, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
+            if (pow2) return dispatch_budget<S, SC, CT, true, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
+            return dispatch_budget<S, SC, CT, false, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
+        }
+    } else {
+        if (p->w == 8 * sizeof(CT)) {
+            if (pow2) return dispatch_budget<S, SC, CT, true, Arith::FULL>(a, pl, dv, ws, d, tau_max, epoch, st);
+            return dispatch_budget<S, SC, CT, false, Arith::FULL>(a, pl, dv, ws, d, tau_max, epoch, st);
         }
     }
-    if (p->w == bits) {
-        if (pow2) return dispatch_budget<S, CT, true, Arith::FULL>(a, pl, dv, ws, d, tau_max, epoch, st);
-        return dispatch_budget<S, CT, false, Arith::FULL>(a, pl, dv, ws, d, tau_max, epoch, st);
-    }
-    if (pow2) return dispatch_budget<S, CT, true, Arith::NARROW>(a, pl, dv, ws, d, tau_max, epoch, st);
-    return dispatch_budget<S, CT, false, Arith::NARROW>(a, pl, dv, ws, d, tau_max, epoch, st);
+    if (pow2) return dispatch_budget<S, SC, CT, true, Arith::NARROW>(a, pl, dv, ws, d, tau_max, epoch, st);
+    return dispatch_budget<S, SC, CT, false, Arith::NARROW>(a, pl, dv, ws, d, tau_max, epoch, st);
 }
 
 rasp::Side side_of(const rasp_batch *b)
@@ -280,18 +281,22 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.tau_max = tau_max;
     a.fresh = (flags & RASP_FRESH) ? 1 : 0;
     a.inplace = (in->iw == out->iw) ? 1 : 0;
-    a.tile_cells = uint32_t(tile_cells(p));
+    a.tile_rows = uint32_t(tile_rows(p));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
 
-    if (p->w <= 32) {
+    if (p->w <= 16) {
         switch (wb) {
-        case 1: return dispatch_flags<uint8_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
-        case 2: return dispatch_flags<uint16_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
-        case 4: return dispatch_flags<uint32_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
-        default: return dispatch_flags<uint64_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+        case 1: return dispatch_flags<uint8_t, uint16_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+        case 2: return dispatch_flags<uint16_t, uint16_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+        case 4: return dispatch_flags<uint32_t, uint16_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+        default: return dispatch_flags<uint64_t, uint16_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
         }
     }
-    return dispatch_flags<uint64_t, uint64_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+    if (p->w <= 32) {
+        if (wb == 4) return dispatch_flags<uint32_t, uint32_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+        return dispatch_flags<uint64_t, uint32_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+    }
+    return dispatch_flags<uint64_t, uint64_t, uint64_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
 }
 
 int rasp_histogram(const int8_t *status, const int64_t *tau_h, uint64_t d, int64_t *out, void *stream)

@@ -4,18 +4,22 @@
 // bit-exact with raspvisor/hypervisor.py:72-164 (_advance/_worker).
 //
 // Execution model:
-//   * one machine per lane; i, a, u0, y0 and the step bookkeeping live in
-//     registers for a whole epoch of K steps;
-//   * each warp owns a private shared-memory tile: M (n rows), the input
-//     tape u[1..ell] (ell+1 rows, one pad row) and s output rows, 32 lanes per row, so lane L's
-//     cell k sits at tile[k*32 + L] -- bank = lane for every data-dependent
-//     address, i.e. conflict-free random access;
+//   * one machine per lane; i, a and the cursor addresses live in registers
+//     for a whole epoch of K steps;
+//   * each warp owns a private shared-memory tile with one row per machine
+//     cell and 32 lanes per row: M (n rows), the input tape u[1..ell] (ell+1
+//     rows, one pad row) and s output rows.  Cells are SC = u16/u32/u64
+//     (the smallest of those holding w bits), lane-interleaved at SC
+//     granularity: lane L's cell k is at row k, column L.  For SC >= 4 bytes
+//     every data-dependent access is bank-conflict-free; u16 cells pack two
+//     lanes per bank word (at most 2-way conflicts) to double the machines
+//     resident per SM;
 //   * the output tape y is write-only during a run: appended cells collect in
 //     tile rows and are flushed to HBM at the end of the epoch;
-//   * opcode dispatch is a predicated select over all candidates (no
-//     branch on the opcode); the fixed-point test uses the equivalent short
-//     form of hv:115 for w >= 2 and the full five-candidate
-//     equality for w = 1;
+//   * opcode dispatch is a predicated select over all candidates (no branch
+//     on the opcode); the fixed-point test uses the equivalent short form of
+//     hv:115 for w >= 2 and the full five-candidate equality
+//     for w = 1;
 //   * a warp leaves the epoch early when __any_sync says no lane is live;
 //   * epochs are separated by stream compaction: survivors are appended to
 //     the next live list (warp-aggregated atomics), finished machines retire.
@@ -68,7 +72,7 @@ struct EpochArgs {
     uint32_t first;                // read the batch from `in`
     uint32_t fresh;                // status=0, steps=0, tau_h=-1 on input
     uint32_t inplace;              // in == out
-    uint32_t tile_cells;           // n + ell + 1 + s
+    uint32_t tile_rows;            // n + ell + 1 + s
 };
 
 template <class CT, Arith AR>
@@ -93,32 +97,32 @@ __device__ __forceinline__ uint32_t modn(CT x, const Geo &g)
 }
 
 // --- per-lane row movement between HBM (element S, contiguous) and the
-//     lane's shared-memory column (element CT, stride 32) --------------------
+//     lane's tile column (element SC, stride 32 cells) ------------------------
 
-template <class S, class CT>
-__device__ __forceinline__ void put16(CT *col, uint32_t k, const uint4 q)
+template <class S, class SC>
+__device__ __forceinline__ void put16(SC *col, uint32_t k, const uint4 q)
 {
     const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
         if constexpr (sizeof(S) == 1) {
 #pragma unroll
-            for (int b = 0; b < 4; ++b) col[(k + 4 * e + b) * 32] = static_cast<CT>((wv[e] >> (8 * b)) & 0xffu);
+            for (int b = 0; b < 4; ++b) col[(k + 4 * e + b) * 32] = static_cast<SC>((wv[e] >> (8 * b)) & 0xffu);
         } else if constexpr (sizeof(S) == 2) {
-            col[(k + 2 * e) * 32] = static_cast<CT>(wv[e] & 0xffffu);
-            col[(k + 2 * e + 1) * 32] = static_cast<CT>(wv[e] >> 16);
+            col[(k + 2 * e) * 32] = static_cast<SC>(wv[e] & 0xffffu);
+            col[(k + 2 * e + 1) * 32] = static_cast<SC>(wv[e] >> 16);
         } else if constexpr (sizeof(S) == 4) {
-            col[(k + e) * 32] = static_cast<CT>(wv[e]);
+            col[(k + e) * 32] = static_cast<SC>(wv[e]);
         } else {
             if (e & 1) continue;
-            col[(k + e / 2) * 32] = static_cast<CT>(static_cast<uint64_t>(wv[e]) |
+            col[(k + e / 2) * 32] = static_cast<SC>(static_cast<uint64_t>(wv[e]) |
                                                     (static_cast<uint64_t>(wv[e + 1]) << 32));
         }
     }
 }
 
-template <class S, class CT>
-__device__ __forceinline__ uint4 get16(const CT *col, uint32_t k)
+template <class S, class SC>
+__device__ __forceinline__ uint4 get16(const SC *col, uint32_t k)
 {
     uint32_t wv[4];
 #pragma unroll
@@ -141,26 +145,26 @@ __device__ __forceinline__ uint4 get16(const CT *col, uint32_t k)
     return make_uint4(wv[0], wv[1], wv[2], wv[3]);
 }
 
-template <class S, class CT>
-__device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t ncells, CT *col)
+template <class S, class SC>
+__device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t ncells, SC *col)
 {
     constexpr uint32_t PER = 16 / sizeof(S);
     uint32_t k = 0;
     if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
         const uint4 *v = reinterpret_cast<const uint4 *>(row);
-        for (; k + PER <= ncells; k += PER) put16<S, CT>(col, k, v[k / PER]);
+        for (; k + PER <= ncells; k += PER) put16<S, SC>(col, k, v[k / PER]);
     }
-    for (; k < ncells; ++k) col[k * 32] = static_cast<CT>(row[k]);
+    for (; k < ncells; ++k) col[k * 32] = static_cast<SC>(row[k]);
 }
 
-template <class S, class CT>
-__device__ __forceinline__ void store_row(S *__restrict__ row, uint32_t ncells, const CT *col)
+template <class S, class SC>
+__device__ __forceinline__ void store_row(S *__restrict__ row, uint32_t ncells, const SC *col)
 {
     constexpr uint32_t PER = 16 / sizeof(S);
     uint32_t k = 0;
     if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
         uint4 *v = reinterpret_cast<uint4 *>(row);
-        for (; k + PER <= ncells; k += PER) v[k / PER] = get16<S, CT>(col, k);
+        for (; k + PER <= ncells; k += PER) v[k / PER] = get16<S, SC>(col, k);
     }
     for (; k < ncells; ++k) row[k] = static_cast<S>(col[k * 32]);
 }
@@ -173,18 +177,17 @@ __device__ __forceinline__ void copy_cells(S *__restrict__ dst, const S *__restr
 
 // --- one machine per lane -------------------------------------------------------
 //
-// Tile layout per warp (byte offsets from the warp's tile base `tb`, cells of
-// type CT, 32 lanes per row, lane L at +L*sizeof(CT)):
+// Tile layout per warp: row r holds cell r of all 32 lanes (SC each).
 //   rows [0, n)            M
 //   rows [n, n+ell+1)      u[1..ell] + one pad row (u[u0+1] is read every step)
-//   rows [n+ell+1, +s)     y[1..s] written during this epoch (flushed at its end)
-// Cursors are kept as byte offsets (ua = U + u0*row, ya = Y + y0*row) so the
-// hot loop does no address arithmetic for them.
+//   rows [n+ell+1, +s)     y[1..s] appended during this epoch (flushed at its end)
+// Cursors are kept as addresses (ua = &u[u0+1], ya = &y[y0+1] of this lane) so
+// the hot loop does no address arithmetic for them.
 
 template <class CT>
 struct LaneState {
     CT i, a;
-    uint32_t ua, ya;  // addresses of u[u0+1] and y[y0+1] in the tile
+    uint32_t ua, ya;  // addresses of u[u0+1] and y[y0+1]
     uint32_t rem;     // remaining budget at epoch start (clamped)
     uint32_t tfin;    // verdict time within the epoch (| kExhaustBit), or kNoVerdict
     bool active;
@@ -193,35 +196,41 @@ struct LaneState {
 // Cell access.  SMEM kernels address the warp tile with 32-bit shared-window
 // addresses (one LDS/STS with a register address per access); the huge-n
 // fallback uses byte offsets from the warp's HBM tile `base`.
-template <class CT, bool SMEM>
+template <class SC, class CT, bool SMEM>
 __device__ __forceinline__ CT ld_cell(char *base, uint32_t a)
 {
     if constexpr (SMEM) {
-        if constexpr (sizeof(CT) == 4) {
+        if constexpr (sizeof(SC) == 2) {
+            unsigned short v;
+            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+            return static_cast<CT>(v);
+        } else if constexpr (sizeof(SC) == 4) {
             uint32_t v;
             asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-            return v;
+            return static_cast<CT>(v);
         } else {
             unsigned long long v;
             asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(a));
             return static_cast<CT>(v);
         }
     } else {
-        return *reinterpret_cast<const volatile CT *>(base + a);
+        return static_cast<CT>(*reinterpret_cast<const volatile SC *>(base + a));
     }
 }
 
-template <class CT, bool SMEM>
+template <class SC, class CT, bool SMEM>
 __device__ __forceinline__ void st_cell(char *base, uint32_t a, CT v)
 {
     if constexpr (SMEM) {
-        if constexpr (sizeof(CT) == 4) {
+        if constexpr (sizeof(SC) == 2) {
+            asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(static_cast<unsigned short>(v)) : "memory");
+        } else if constexpr (sizeof(SC) == 4) {
             asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(static_cast<uint32_t>(v)) : "memory");
         } else {
             asm volatile("st.shared.u64 [%0], %1;" ::"r"(a), "l"(static_cast<unsigned long long>(v)) : "memory");
         }
     } else {
-        *reinterpret_cast<volatile CT *>(base + a) = v;
+        *reinterpret_cast<volatile SC *>(base + a) = static_cast<SC>(v);
     }
 }
 
@@ -232,11 +241,11 @@ __device__ __forceinline__ void st_cell(char *base, uint32_t a, CT v)
 // taken to its own address.  BUDGET: check t == rem inside the loop (runs
 // whose machines did not all start at the same step count); the final,
 // non-applying evaluation at t == K always checks it.
-template <class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
+template <class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
 __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
                                           uint32_t yend, const Geo &g, uint32_t t, bool can_apply)
 {
-    constexpr uint32_t SH = sizeof(CT) == 4 ? 7 : 8;   // log2(row bytes)
+    constexpr uint32_t SH = sizeof(SC) == 2 ? 6 : sizeof(SC) == 4 ? 7 : 8;   // log2(row bytes)
     constexpr uint32_t ROW = 1u << SH;
     const CT mask = static_cast<CT>(g.mask);
     uint32_t ia, ib;
@@ -247,11 +256,11 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
         ia = modn<CT, POW2>(L.i, g);
         ib = modn<CT, POW2>(wrap<CT, AR>(L.i + 1, mask), g);
     }
-    const CT o = ld_cell<CT, SMEM>(base, (ia << SH) + lm);
-    const CT jw = ld_cell<CT, SMEM>(base, (ib << SH) + lm);
+    const CT o = ld_cell<SC, CT, SMEM>(base, (ia << SH) + lm);
+    const CT jw = ld_cell<SC, CT, SMEM>(base, (ib << SH) + lm);
     const uint32_t jo = (modn<CT, POW2>(jw, g) << SH) + lm;
-    const CT mj = ld_cell<CT, SMEM>(base, jo);
-    const CT ud = ld_cell<CT, SMEM>(base, L.ua);
+    const CT mj = ld_cell<SC, CT, SMEM>(base, jo);
+    const CT ud = ld_cell<SC, CT, SMEM>(base, L.ua);
     const CT a0 = L.a;
 
     const bool rd = (o == 6) & (L.ua < uend);
@@ -287,54 +296,44 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
         L.i = ni;
         L.a = na;
     }
-    if (app & ((o == 4) | rd)) st_cell<CT, SMEM>(base, jo, nm);
+    if (app & ((o == 4) | rd)) st_cell<SC, CT, SMEM>(base, jo, nm);
     const bool wy = app & pri;
-    if (wy) st_cell<CT, SMEM>(base, L.ya, mj);
+    if (wy) st_cell<SC, CT, SMEM>(base, L.ya, mj);
     if (app & rd) L.ua += ROW;
     if (wy) L.ya += ROW;
 }
 
-template <class S, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
-__global__ void __launch_bounds__(128)
-epoch_kernel(const EpochArgs A, CT *gtiles)
+template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
+__global__ void __launch_bounds__(128, SMEM ? 10 : 1)
+epoch_kernel(const EpochArgs A, SC *gtiles)
 {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr uint32_t ROW = 32 * sizeof(CT);
+    constexpr uint32_t ROW = 32 * sizeof(SC);
     const uint32_t lane = threadIdx.x & 31;
     const uint32_t wib = threadIdx.x >> 5;
-    const Geo g = A.g;
-    const uint32_t n = g.n;
-    const uint64_t ucols = static_cast<uint64_t>(g.ell) + 1;
-    const uint64_t ycols = static_cast<uint64_t>(g.s) + 1;
-    const uint32_t tile_bytes = A.tile_cells * ROW;
+    const uint32_t n = A.g.n;
+    const uint32_t tile_bytes = A.tile_rows * ROW;
 
     char *tb;      // SMEM: the dynamic shared window; else the warp's HBM tile
     uint32_t lm;   // address of this lane's column in row 0
     if constexpr (SMEM) {
         tb = reinterpret_cast<char *>(smem_raw);
         lm = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes +
-             lane * static_cast<uint32_t>(sizeof(CT));
+             lane * static_cast<uint32_t>(sizeof(SC));
     } else {
         tb = reinterpret_cast<char *>(gtiles) +
              (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * static_cast<size_t>(tile_bytes);
-        lm = lane * static_cast<uint32_t>(sizeof(CT));
+        lm = lane * static_cast<uint32_t>(sizeof(SC));
     }
     const uint32_t U = n * ROW + lm;                       // u[1] of this lane
-    const uint32_t Y = (n + g.ell + 1) * ROW + lm;         // y[1] of this lane (epoch scratch)
-    const uint32_t uend = U + g.ell * ROW;
-    const uint32_t yend = Y + g.s * ROW;
-    // generic pointers to this lane's columns, for the (cold) row copies
+    const uint32_t Y = (n + A.g.ell + 1) * ROW + lm;       // y[1] of this lane (epoch scratch)
+    // generic base for the (cold) row copies: gb + address = generic pointer
     char *gb = SMEM ? reinterpret_cast<char *>(smem_raw) -
                           static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw))
                     : tb;
-    CT *colM = reinterpret_cast<CT *>(gb + lm);
-    CT *colU = reinterpret_cast<CT *>(gb + U);
-    CT *colY = reinterpret_cast<CT *>(gb + Y);
 
     const uint32_t count = A.count_in_ptr ? *A.count_in_ptr : A.count_in;
     const uint32_t ntiles = (count + 31) / 32;
-    const Side &src = A.first ? A.in : A.out;
-    const Side &dst = A.out;
     const bool copy_side = A.first && !A.inplace;
     const bool fresh = A.fresh != 0;
 
@@ -343,86 +342,106 @@ epoch_kernel(const EpochArgs A, CT *gtiles)
         if (lane == 0) tix = atomicAdd(A.tile_ctr, 1u);
         tix = __shfl_sync(kFull, tix, 0);
         if (tix >= ntiles) break;
-        const uint32_t j = tix * 32 + lane;
-        const bool valid = j < count;
-        const uint64_t id = valid ? (A.list_in ? A.list_in[j] : j) : 0;
 
         LaneState<CT> L;
-        L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tfin = kNoVerdict;
-        bool running = valid;
-        int64_t steps0 = fresh ? A.covered : 0;
-        if (valid && !fresh) {
-            if (A.first) {
-                const int8_t st = A.in.status[id];
-                const int64_t s0 = A.in.steps[id];
-                if (st != kRunning) running = false;
-                steps0 = s0;
-                if (copy_side) {
-                    dst.status[id] = st;
-                    dst.steps[id] = s0;
-                    dst.tau_h[id] = A.in.tau_h[id];
+        bool running;
+        {   // ---- load phase (values here are not kept live across the step loop)
+            const Side &src = A.first ? A.in : A.out;
+            const Side &dst = A.out;
+            const uint64_t ucols = static_cast<uint64_t>(A.g.ell) + 1;
+            const uint64_t ycols = static_cast<uint64_t>(A.g.s) + 1;
+            const uint32_t j = tix * 32 + lane;
+            const bool valid = j < count;
+            const uint64_t id = valid ? (A.list_in ? A.list_in[j] : j) : 0;
+            running = valid;
+            int64_t steps0 = fresh ? A.covered : 0;
+            if (valid && !fresh) {
+                if (A.first) {
+                    const int8_t st = A.in.status[id];
+                    const int64_t s0 = A.in.steps[id];
+                    if (st != kRunning) running = false;
+                    steps0 = s0;
+                    if (copy_side) {
+                        dst.status[id] = st;
+                        dst.steps[id] = s0;
+                        dst.tau_h[id] = A.in.tau_h[id];
+                    }
+                } else {
+                    steps0 = dst.steps[id];
                 }
-            } else {
-                steps0 = dst.steps[id];
             }
-        }
-        const S *srcM = static_cast<const S *>(src.M) + id * n;
-        const S *srcU = static_cast<const S *>(src.u) + id * ucols;
-        const S *srcY = static_cast<const S *>(src.y) + id * ycols;
-        if (valid && copy_side && !running) {
-            // untouched machine, out-of-place: carry it over verbatim
-            static_cast<S *>(dst.iw)[id] = static_cast<const S *>(A.in.iw)[id];
-            static_cast<S *>(dst.ac)[id] = static_cast<const S *>(A.in.ac)[id];
-            copy_cells(static_cast<S *>(dst.M) + id * n, srcM, n);
-            copy_cells(static_cast<S *>(dst.u) + id * ucols, srcU, ucols);
-            copy_cells(static_cast<S *>(dst.y) + id * ycols, srcY, ycols);
-        }
-        uint32_t y0_start = 0;
-        if (running) {
-            L.i = static_cast<CT>(static_cast<const S *>(src.iw)[id]);
-            L.a = static_cast<CT>(static_cast<const S *>(src.ac)[id]);
-            L.ua = U + static_cast<uint32_t>(srcU[0]) * ROW;
-            y0_start = static_cast<uint32_t>(srcY[0]);
-            L.ya = Y + y0_start * ROW;
-            load_row<S, CT>(srcM, n, colM);
-            load_row<S, CT>(srcU + 1, g.ell, colU);
-            if (copy_side) {
-                copy_cells(static_cast<S *>(dst.u) + id * ucols + 1, srcU + 1, g.ell);
-                copy_cells(static_cast<S *>(dst.y) + id * ycols + 1, srcY + 1, g.s);
+            const S *srcM = static_cast<const S *>(src.M) + id * n;
+            const S *srcU = static_cast<const S *>(src.u) + id * ucols;
+            const S *srcY = static_cast<const S *>(src.y) + id * ycols;
+            if (valid && copy_side && !running) {
+                // untouched machine, out-of-place: carry it over verbatim
+                static_cast<S *>(dst.iw)[id] = static_cast<const S *>(A.in.iw)[id];
+                static_cast<S *>(dst.ac)[id] = static_cast<const S *>(A.in.ac)[id];
+                copy_cells(static_cast<S *>(dst.M) + id * n, srcM, n);
+                copy_cells(static_cast<S *>(dst.u) + id * ucols, srcU, ucols);
+                copy_cells(static_cast<S *>(dst.y) + id * ycols, srcY, ycols);
             }
+            L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tfin = kNoVerdict;
+            if (running) {
+                L.i = static_cast<CT>(static_cast<const S *>(src.iw)[id]);
+                L.a = static_cast<CT>(static_cast<const S *>(src.ac)[id]);
+                L.ua = U + static_cast<uint32_t>(srcU[0]) * ROW;
+                L.ya = Y + static_cast<uint32_t>(srcY[0]) * ROW;
+                load_row<S, SC>(srcM, n, reinterpret_cast<SC *>(gb + lm));
+                load_row<S, SC>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
+                if (copy_side) {
+                    copy_cells(static_cast<S *>(dst.u) + id * ucols + 1, srcU + 1, A.g.ell);
+                    copy_cells(static_cast<S *>(dst.y) + id * ycols + 1, srcY + 1, A.g.s);
+                }
+            }
+            const uint64_t rem64 = (steps0 >= A.tau_max) ? 0ull
+                                                         : static_cast<uint64_t>(A.tau_max - steps0);
+            L.rem = rem64 > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(rem64);
+            L.active = running;
         }
-        const uint64_t rem64 = (steps0 >= A.tau_max) ? 0ull
-                                                     : static_cast<uint64_t>(A.tau_max - steps0);
-        L.rem = rem64 > 0xffffffffull ? 0xffffffffu : static_cast<uint32_t>(rem64);
-        L.active = running;
         asm volatile("" ::: "memory");   // column fills above are visible to the asm loads below
 
-        const uint32_t K = A.K;
-        uint32_t t = 0;
-        bool live = __any_sync(kFull, L.active);
-        for (; live && t + 2 <= K; t += 2) {
-            rasp_step<CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t, true);
-            rasp_step<CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t + 1, true);
-            live = __any_sync(kFull, L.active);
+        {   // ---- step loop
+            const Geo g = A.g;
+            const uint32_t uend = U + g.ell * ROW;
+            const uint32_t yend = Y + g.s * ROW;
+            const uint32_t K = A.K;
+            uint32_t t = 0;
+            bool live = __any_sync(kFull, L.active);
+            for (; live && t + 2 <= K; t += 2) {
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t, true);
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t + 1, true);
+                live = __any_sync(kFull, L.active);
+            }
+            if (live && t < K) {
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t, true);
+                ++t;
+                live = __any_sync(kFull, L.active);
+            }
+            if (live) rasp_step<SC, CT, POW2, AR, true, SMEM>(L, tb, lm, uend, yend, g, K, false);
         }
-        if (live && t < K) {
-            rasp_step<CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t, true);
-            ++t;
-            live = __any_sync(kFull, L.active);
-        }
-        if (live) rasp_step<CT, POW2, AR, true, SMEM>(L, tb, lm, uend, yend, g, K, false);
 
         bool survivor = false;
-        if (running) {
+        uint32_t sid = 0;
+        if (running) {   // ---- write-back phase (re-derives what the load phase knew)
+            const Side &src = A.first ? A.in : A.out;
+            const Side &dst = A.out;
+            const uint64_t ucols = static_cast<uint64_t>(A.g.ell) + 1;
+            const uint64_t ycols = static_cast<uint64_t>(A.g.s) + 1;
+            const uint32_t j = tix * 32 + lane;
+            const uint64_t id = A.list_in ? A.list_in[j] : j;
+            const int64_t steps0 = fresh ? A.covered : (A.first ? A.in.steps[id] : dst.steps[id]);
+            const uint32_t y0_start = static_cast<uint32_t>(static_cast<const S *>(src.y)[id * ycols]);
             const uint32_t u0 = (L.ua - U) / ROW;
             const uint32_t y0 = (L.ya - Y) / ROW;
             S *dY = static_cast<S *>(dst.y) + id * ycols;
+            const SC *colY = reinterpret_cast<const SC *>(gb + Y);
+            for (uint32_t k = y0_start; k < y0; ++k) dY[k + 1] = static_cast<S>(colY[k * 32]);
+            dY[0] = static_cast<S>(y0);
             static_cast<S *>(dst.iw)[id] = static_cast<S>(L.i);
             static_cast<S *>(dst.ac)[id] = static_cast<S>(L.a);
             static_cast<S *>(dst.u)[id * ucols] = static_cast<S>(u0);
-            dY[0] = static_cast<S>(y0);
-            for (uint32_t k = y0_start; k < y0; ++k) dY[k + 1] = static_cast<S>(colY[k * 32]);
-            store_row<S, CT>(static_cast<S *>(dst.M) + id * n, n, colM);
+            store_row<S, SC>(static_cast<S *>(dst.M) + id * n, n, reinterpret_cast<const SC *>(gb + lm));
             if (L.tfin != kNoVerdict) {
                 const int64_t tend = steps0 + (L.tfin & ~kExhaustBit);
                 dst.steps[id] = tend;
@@ -435,7 +454,8 @@ epoch_kernel(const EpochArgs A, CT *gtiles)
                 }
             } else {
                 survivor = true;
-                if (!fresh) dst.steps[id] = steps0 + K;
+                sid = static_cast<uint32_t>(id);
+                if (!fresh) dst.steps[id] = steps0 + A.K;
             }
         }
         const unsigned sv = __ballot_sync(kFull, survivor);
@@ -443,7 +463,7 @@ epoch_kernel(const EpochArgs A, CT *gtiles)
             uint32_t base = 0;
             if (lane == 0) base = atomicAdd(A.count_out, static_cast<uint32_t>(__popc(sv)));
             base = __shfl_sync(kFull, base, 0);
-            if (survivor) A.list_out[base + __popc(sv & ((1u << lane) - 1u))] = static_cast<uint32_t>(id);
+            if (survivor) A.list_out[base + __popc(sv & ((1u << lane) - 1u))] = sid;
         }
     }
 }
