@@ -283,6 +283,18 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.inplace = (in->iw == out->iw) ? 1 : 0;
     a.tile_rows = uint32_t(tile_rows(p));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    if (!a.inplace) {
+        // out-of-place: the input tapes and the bookkeeping arrays move in bulk;
+        // the kernels then treat `out` as the working copy
+        const size_t ub = size_t(d) * (p->ell + 1) * wb, yb = size_t(d) * (p->s + 1) * wb;
+        RASP_CUDA(cudaMemcpyAsync(out->u, in->u, ub, cudaMemcpyDeviceToDevice, st));
+        RASP_CUDA(cudaMemcpyAsync(out->y, in->y, yb, cudaMemcpyDeviceToDevice, st));
+        if (!a.fresh) {
+            RASP_CUDA(cudaMemcpyAsync(out->status, in->status, size_t(d), cudaMemcpyDeviceToDevice, st));
+            RASP_CUDA(cudaMemcpyAsync(out->steps, in->steps, size_t(d) * 8, cudaMemcpyDeviceToDevice, st));
+            RASP_CUDA(cudaMemcpyAsync(out->tau_h, in->tau_h, size_t(d) * 8, cudaMemcpyDeviceToDevice, st));
+        }
+    }
 
     if (p->w <= 16) {
         switch (wb) {

@@ -263,25 +263,22 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
     const CT ud = ld_cell<SC, CT, SMEM>(base, L.ua);
     const CT a0 = L.a;
 
-    const bool rd = (o == 6) & (L.ua < uend);
+    const bool e6 = (o == 6);
+    const bool rd = e6 & (L.ua < uend);
     const bool taken = (o == 5) & (a0 != 0);
     const bool pri = (o == 7) & (L.ya < yend);
     const CT i2 = wrap<CT, AR>(L.i + 2, mask);
-    CT na = (o == 1) ? jw : a0;
-    na = (o == 2) ? static_cast<CT>(a0 + mj) : na;
-    na = (o == 3) ? static_cast<CT>(a0 * mj) : na;
-    na = wrap<CT, AR>(na, mask);
-    const CT nm = (o == 4) ? a0 : ud;
     bool fixed;
-    CT ni;
     if constexpr (AR != Arith::W1) {
-        fixed = (o == 0) | (o > 7) | ((o == 6) & !rd) | (taken & (jw == L.i));
-        ni = taken ? jw : i2;
+        fixed = (static_cast<CT>(o - 1) > 6) | (e6 & !rd) | (taken & (jw == L.i));
     } else {
         const bool adv = (static_cast<CT>(o - 1) < 4) | ((o == 5) & (a0 == 0)) | rd | (o == 7);
-        ni = taken ? jw : (adv ? i2 : L.i);
-        const CT nmf = ((o == 4) | rd) ? nm : mj;
-        fixed = (ni == L.i) & (na == a0) & (nmf == mj) & !rd & !pri;
+        const CT nif = taken ? jw : (adv ? i2 : L.i);
+        CT naf = (o == 1) ? jw : a0;
+        naf = (o == 2) ? wrap<CT, AR>(a0 + mj, mask) : naf;
+        naf = (o == 3) ? wrap<CT, AR>(a0 * mj, mask) : naf;
+        const CT nmf = (o == 4) ? a0 : (rd ? ud : mj);
+        fixed = (nif == L.i) & (naf == a0) & (nmf == mj) & !rd & !pri;
     }
     if (BUDGET || !can_apply) {
         const bool fin = L.active & (fixed | (t == L.rem));
@@ -292,15 +289,20 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
         L.active = L.active & !fixed;
     }
     const bool app = L.active & can_apply;
-    if (app) {
-        L.i = ni;
-        L.a = na;
+    // commit: every update is a predicated move/store keyed on its own case
+    if (app & (o == 1)) L.a = jw;
+    if (app & (o == 2)) L.a = wrap<CT, AR>(a0 + mj, mask);
+    if (app & (o == 3)) L.a = wrap<CT, AR>(a0 * mj, mask);
+    if (app & (o == 4)) st_cell<SC, CT, SMEM>(base, jo, a0);
+    if (app & rd) {
+        st_cell<SC, CT, SMEM>(base, jo, ud);
+        L.ua += ROW;
     }
-    if (app & ((o == 4) | rd)) st_cell<SC, CT, SMEM>(base, jo, nm);
-    const bool wy = app & pri;
-    if (wy) st_cell<SC, CT, SMEM>(base, L.ya, mj);
-    if (app & rd) L.ua += ROW;
-    if (wy) L.ya += ROW;
+    if (app & pri) {
+        st_cell<SC, CT, SMEM>(base, L.ya, mj);
+        L.ya += ROW;
+    }
+    if (app) L.i = taken ? jw : i2;
 }
 
 template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
@@ -337,11 +339,12 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     const bool copy_side = A.first && !A.inplace;
     const bool fresh = A.fresh != 0;
 
+    uint32_t next = 0;   // lane 0: the tile this warp takes next (claimed one tile ahead)
+    if (lane == 0) next = atomicAdd(A.tile_ctr, 1u);
     for (;;) {
-        uint32_t tix = 0;
-        if (lane == 0) tix = atomicAdd(A.tile_ctr, 1u);
-        tix = __shfl_sync(kFull, tix, 0);
+        const uint32_t tix = __shfl_sync(kFull, next, 0);
         if (tix >= ntiles) break;
+        if (lane == 0) next = atomicAdd(A.tile_ctr, 1u);
 
         LaneState<CT> L;
         bool running;
@@ -356,30 +359,20 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             running = valid;
             int64_t steps0 = fresh ? A.covered : 0;
             if (valid && !fresh) {
-                if (A.first) {
-                    const int8_t st = A.in.status[id];
-                    const int64_t s0 = A.in.steps[id];
-                    if (st != kRunning) running = false;
-                    steps0 = s0;
-                    if (copy_side) {
-                        dst.status[id] = st;
-                        dst.steps[id] = s0;
-                        dst.tau_h[id] = A.in.tau_h[id];
-                    }
-                } else {
-                    steps0 = dst.steps[id];
-                }
+                // status/steps/tau_h of `out` already hold the input values (the
+                // host copies them for out-of-place runs before the first epoch)
+                if (A.first && dst.status[id] != kRunning) running = false;
+                steps0 = dst.steps[id];
             }
             const S *srcM = static_cast<const S *>(src.M) + id * n;
             const S *srcU = static_cast<const S *>(src.u) + id * ucols;
             const S *srcY = static_cast<const S *>(src.y) + id * ycols;
             if (valid && copy_side && !running) {
-                // untouched machine, out-of-place: carry it over verbatim
+                // untouched machine, out-of-place: carry i, a, M over (u, y were
+                // copied in bulk by the host)
                 static_cast<S *>(dst.iw)[id] = static_cast<const S *>(A.in.iw)[id];
                 static_cast<S *>(dst.ac)[id] = static_cast<const S *>(A.in.ac)[id];
                 copy_cells(static_cast<S *>(dst.M) + id * n, srcM, n);
-                copy_cells(static_cast<S *>(dst.u) + id * ucols, srcU, ucols);
-                copy_cells(static_cast<S *>(dst.y) + id * ycols, srcY, ycols);
             }
             L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tfin = kNoVerdict;
             if (running) {
@@ -389,10 +382,6 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 L.ya = Y + static_cast<uint32_t>(srcY[0]) * ROW;
                 load_row<S, SC>(srcM, n, reinterpret_cast<SC *>(gb + lm));
                 load_row<S, SC>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
-                if (copy_side) {
-                    copy_cells(static_cast<S *>(dst.u) + id * ucols + 1, srcU + 1, A.g.ell);
-                    copy_cells(static_cast<S *>(dst.y) + id * ycols + 1, srcY + 1, A.g.s);
-                }
             }
             const uint64_t rem64 = (steps0 >= A.tau_max) ? 0ull
                                                          : static_cast<uint64_t>(A.tau_max - steps0);
@@ -430,7 +419,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const uint64_t ycols = static_cast<uint64_t>(A.g.s) + 1;
             const uint32_t j = tix * 32 + lane;
             const uint64_t id = A.list_in ? A.list_in[j] : j;
-            const int64_t steps0 = fresh ? A.covered : (A.first ? A.in.steps[id] : dst.steps[id]);
+            const int64_t steps0 = fresh ? A.covered : dst.steps[id];
             const uint32_t y0_start = static_cast<uint32_t>(static_cast<const S *>(src.y)[id * ycols]);
             const uint32_t u0 = (L.ua - U) / ROW;
             const uint32_t y0 = (L.ya - Y) / ROW;
