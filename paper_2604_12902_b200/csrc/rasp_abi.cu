@@ -28,8 +28,8 @@ int cuda_fail(cudaError_t e, const char *what)
         if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
     } while (0)
 
-constexpr int kMaxEpochs = 1024;        // counter slots in the workspace
-constexpr int kPollAfter = 24;          // epochs after which the host polls the live count
+using rasp::kMaxEpochs;                 // schedule slots in the workspace
+constexpr int kPollAfter = 24;          // epochs after which the host polls the schedule
 constexpr uint32_t kMaxK = 1u << 24;    // longest epoch, in steps
 constexpr int kWarpsPerBlockMax = 4;
 constexpr size_t kGlobalTileBudget = size_t(1) << 30;  // bytes of HBM tiles for huge n
@@ -100,7 +100,7 @@ void plan_shape(const rasp_params *p, const Device &dv, Plan &pl)
 
 struct Workspace {
     uint32_t *lists[2];
-    uint32_t *counters;   // [kMaxEpochs][2]: tile counter, live count
+    rasp::Sched *sched;
     void *gtiles;
 };
 
@@ -113,8 +113,8 @@ size_t workspace_layout(const rasp_params *p, uint64_t d, const Plan &pl, void *
     off += list_bytes;
     if (ws) ws->lists[1] = reinterpret_cast<uint32_t *>(b + off);
     off += list_bytes;
-    if (ws) ws->counters = reinterpret_cast<uint32_t *>(b + off);
-    off += align256(sizeof(uint32_t) * 2 * kMaxEpochs);
+    if (ws) ws->sched = reinterpret_cast<rasp::Sched *>(b + off);
+    off += align256(sizeof(rasp::Sched));
     if (ws) ws->gtiles = pl.gtile_bytes ? b + off : nullptr;
     off += align256(pl.gtile_bytes);
     (void)p;
@@ -138,35 +138,40 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
     const uint64_t need_blocks = (tiles + pl.warps_per_block - 1) / pl.warps_per_block;
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(pl.blocks), need_blocks)));
 
-    RASP_CUDA(cudaMemsetAsync(ws.counters, 0, sizeof(uint32_t) * 2 * kMaxEpochs, st));
-    int64_t covered = 0;
-    uint64_t K = uint64_t(std::max<int64_t>(epoch, 1));
+    RASP_CUDA(cudaMemsetAsync(ws.sched, 0, sizeof(rasp::Sched), st));
+    // Enough launches for the pure doubling schedule; the device schedule can
+    // only finish sooner (it lengthens epochs once survivors stop halting).
+    const uint64_t K0 = uint64_t(std::min<int64_t>(std::max<int64_t>(epoch, 1), tau_max));
+    int planned = 1;
+    {
+        uint64_t cov = K0, k = std::max<uint64_t>(K0, 1);
+        while (int64_t(cov) < tau_max && planned < kPollAfter) {
+            k = std::min<uint64_t>(k * 2, kMaxK);
+            cov += k;
+            ++planned;
+        }
+    }
     for (int e = 0;; ++e) {
         if (e >= kMaxEpochs) return RASP_ECAPACITY;
-        if (e >= kPollAfter) {
-            uint32_t live = 0;
-            RASP_CUDA(cudaMemcpyAsync(&live, ws.counters + 2 * (e - 1) + 1, sizeof live,
-                                      cudaMemcpyDeviceToHost, st));
+        if (e >= planned) {
+            // long budgets: ask the device whether another epoch is needed
+            uint32_t knext = 0;
+            RASP_CUDA(cudaMemcpyAsync(&knext, &ws.sched->K[e], sizeof knext, cudaMemcpyDeviceToHost, st));
             RASP_CUDA(cudaStreamSynchronize(st));
-            if (live == 0) break;
+            if (knext == 0) break;
         }
         rasp::EpochArgs a = base;
-        const int64_t left = tau_max - covered;
-        a.K = uint32_t(std::min<uint64_t>(K, uint64_t(std::max<int64_t>(left, 0))));
-        a.covered = covered;
+        a.sched = ws.sched;
+        a.e = uint32_t(e);
         a.first = e == 0;
+        a.count_in = uint32_t(d);
+        a.K0 = uint32_t(K0);
+        a.kmax = kMaxK;
         a.list_in = e == 0 ? nullptr : ws.lists[(e - 1) & 1];
-        a.count_in_ptr = e == 0 ? nullptr : ws.counters + 2 * (e - 1) + 1;
-        a.count_in = e == 0 ? uint32_t(d) : 0;
         a.list_out = ws.lists[e & 1];
-        a.tile_ctr = ws.counters + 2 * e;
-        a.count_out = ws.counters + 2 * e + 1;
         kern<<<grid, threads, pl.dyn_smem, st>>>(a, static_cast<SC *>(ws.gtiles));
         RASP_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
-        covered += a.K;
-        if (covered >= tau_max) break;
-        K = std::min<uint64_t>(K * 2, kMaxK);
     }
     return RASP_OK;
 }

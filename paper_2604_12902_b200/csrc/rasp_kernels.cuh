@@ -57,18 +57,31 @@ struct Side {
     int64_t *tau_h;
 };
 
+constexpr int kMaxEpochs = 1024;
+
+// Device-side epoch schedule (workspace).  Epoch e reads its length K[e] and
+// start offset covered[e]; the last block of epoch e writes K[e+1] from the
+// survival ratio it observed, so the host can enqueue epochs without
+// knowing the halting-time distribution.
+struct Sched {
+    int64_t covered[kMaxEpochs];     // steps every fresh survivor has taken before epoch e
+    uint32_t K[kMaxEpochs];          // applying steps in epoch e (0: nothing left)
+    uint32_t count[kMaxEpochs];      // survivors after epoch e
+    uint32_t tile_ctr[kMaxEpochs];
+    uint32_t blocks_done[kMaxEpochs];
+};
+
 struct EpochArgs {
     Geo g;
     Side in, out;
+    Sched *sched;
     const uint32_t *list_in;       // nullptr: identity list 0..count-1 (first epoch)
     uint32_t *list_out;
-    const uint32_t *count_in_ptr;  // nullptr: use count_in
-    uint32_t *count_out;
-    uint32_t *tile_ctr;
     int64_t tau_max;
-    int64_t covered;               // steps every fresh survivor has taken so far
-    uint32_t count_in;
-    uint32_t K;                    // applying steps in this epoch
+    uint32_t e;                    // epoch index
+    uint32_t count_in;             // first epoch: batch size
+    uint32_t K0;                   // first epoch length
+    uint32_t kmax;                 // longest epoch
     uint32_t first;                // read the batch from `in`
     uint32_t fresh;                // status=0, steps=0, tau_h=-1 on input
     uint32_t inplace;              // in == out
@@ -334,17 +347,20 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                           static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw))
                     : tb;
 
-    const uint32_t count = A.count_in_ptr ? *A.count_in_ptr : A.count_in;
-    const uint32_t ntiles = (count + 31) / 32;
+    Sched *sc = A.sched;
+    const uint32_t e = A.e;
+    const uint32_t count = A.first ? A.count_in : sc->count[e - 1];
+    const uint32_t K = A.first ? A.K0 : sc->K[e];
+    const int64_t covered = A.first ? 0 : sc->covered[e];
+    const uint32_t ntiles = (K == 0 && !A.first) ? 0 : (count + 31) / 32;
     const bool copy_side = A.first && !A.inplace;
     const bool fresh = A.fresh != 0;
 
-    uint32_t next = 0;   // lane 0: the tile this warp takes next (claimed one tile ahead)
-    if (lane == 0) next = atomicAdd(A.tile_ctr, 1u);
+    uint32_t next = 0;   // lane 0: the tile this warp takes next
+    if (lane == 0) next = atomicAdd(&sc->tile_ctr[e], 1u);
     for (;;) {
         const uint32_t tix = __shfl_sync(kFull, next, 0);
         if (tix >= ntiles) break;
-        if (lane == 0) next = atomicAdd(A.tile_ctr, 1u);
 
         LaneState<CT> L;
         bool running;
@@ -357,7 +373,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const bool valid = j < count;
             const uint64_t id = valid ? (A.list_in ? A.list_in[j] : j) : 0;
             running = valid;
-            int64_t steps0 = fresh ? A.covered : 0;
+            int64_t steps0 = fresh ? covered : 0;
             if (valid && !fresh) {
                 // status/steps/tau_h of `out` already hold the input values (the
                 // host copies them for out-of-place runs before the first epoch)
@@ -394,7 +410,6 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const Geo g = A.g;
             const uint32_t uend = U + g.ell * ROW;
             const uint32_t yend = Y + g.s * ROW;
-            const uint32_t K = A.K;
             uint32_t t = 0;
             bool live = __any_sync(kFull, L.active);
             for (; live && t + 2 <= K; t += 2) {
@@ -409,6 +424,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             }
             if (live) rasp_step<SC, CT, POW2, AR, true, SMEM>(L, tb, lm, uend, yend, g, K, false);
         }
+        if (lane == 0) next = atomicAdd(&sc->tile_ctr[e], 1u);   // overlaps the write-back
 
         bool survivor = false;
         uint32_t sid = 0;
@@ -419,7 +435,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const uint64_t ycols = static_cast<uint64_t>(A.g.s) + 1;
             const uint32_t j = tix * 32 + lane;
             const uint64_t id = A.list_in ? A.list_in[j] : j;
-            const int64_t steps0 = fresh ? A.covered : dst.steps[id];
+            const int64_t steps0 = fresh ? covered : dst.steps[id];
             const uint32_t y0_start = static_cast<uint32_t>(static_cast<const S *>(src.y)[id * ycols]);
             const uint32_t u0 = (L.ua - U) / ROW;
             const uint32_t y0 = (L.ya - Y) / ROW;
@@ -444,15 +460,41 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             } else {
                 survivor = true;
                 sid = static_cast<uint32_t>(id);
-                if (!fresh) dst.steps[id] = steps0 + A.K;
+                if (!fresh) dst.steps[id] = steps0 + K;
             }
         }
         const unsigned sv = __ballot_sync(kFull, survivor);
         if (sv) {
             uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(A.count_out, static_cast<uint32_t>(__popc(sv)));
+            if (lane == 0) base = atomicAdd(&sc->count[e], static_cast<uint32_t>(__popc(sv)));
             base = __shfl_sync(kFull, base, 0);
             if (survivor) A.list_out[base + __popc(sv & ((1u << lane) - 1u))] = sid;
+        }
+    }
+
+    // the last block to finish plans the next epoch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&sc->blocks_done[e], 1u) == gridDim.x - 1) {
+            __threadfence();
+            const uint32_t cout = atomicAdd(&sc->count[e], 0u);
+            const int64_t cov = covered + K;
+            const int64_t left = A.tau_max - cov;
+            uint32_t kn = 0;
+            if (cout > 0 && left > 0 && ntiles > 0) {
+                // survivors that mostly keep running get the whole remaining
+                // budget in one epoch; otherwise keep compacting at 2x length
+                const bool stable = 4ull * cout >= 3ull * count;
+                const uint64_t want = stable ? static_cast<uint64_t>(left)
+                                             : 2ull * (K > 0 ? K : 1u);
+                kn = static_cast<uint32_t>(min(min(want, static_cast<uint64_t>(left)),
+                                               static_cast<uint64_t>(A.kmax)));
+            }
+            if (e + 1 < kMaxEpochs) {
+                sc->K[e + 1] = kn;
+                sc->covered[e + 1] = cov;
+            }
         }
     }
 }
