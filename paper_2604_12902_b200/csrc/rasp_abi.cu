@@ -208,6 +208,23 @@ int dispatch_flags(const rasp_params *p, const rasp::EpochArgs &a, const Plan &p
     return dispatch_budget<S, SC, CT, false, Arith::NARROW>(a, pl, dv, ws, d, tau_max, epoch, st);
 }
 
+// Device-to-device copy with a kernel (cudaMemcpyAsync D2D would occupy a copy
+// engine that host<->device pipelines need).
+int dev_copy(void *dst, const void *src, size_t bytes, const Device &dv, cudaStream_t st)
+{
+    if (bytes == 0) return RASP_OK;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src);
+    const size_t n16 = (a & 15) ? 0 : bytes / 16;
+    const size_t head = n16 * 16;
+    const unsigned blocks = unsigned(std::max<size_t>(1, std::min<size_t>((n16 + 255) / 256, size_t(dv.nsm) * 8)));
+    rasp::copy_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint4 *>(src), static_cast<uint4 *>(dst), n16,
+                                              static_cast<const unsigned char *>(src) + head,
+                                              static_cast<unsigned char *>(dst) + head, bytes - head);
+    RASP_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return RASP_OK;
+}
+
 rasp::Side side_of(const rasp_batch *b)
 {
     rasp::Side s;
@@ -287,20 +304,23 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.fresh = (flags & RASP_FRESH) ? 1 : 0;
     a.inplace = (in->iw == out->iw) ? 1 : 0;
     a.tile_rows = uint32_t(tile_rows(p));
+    a.one = 1;
+    a.two = 2;
+    a.row = uint32_t(32 * cell_bytes(p->w));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!a.inplace) {
         // out-of-place: the input tapes and the bookkeeping arrays move in bulk;
         // the kernels then treat `out` as the working copy
         const size_t ub = size_t(d) * (p->ell + 1) * wb, yb = size_t(d) * (p->s + 1) * wb;
-        RASP_CUDA(cudaMemcpyAsync(out->u, in->u, ub, cudaMemcpyDeviceToDevice, st));
-        RASP_CUDA(cudaMemcpyAsync(out->y, in->y, yb, cudaMemcpyDeviceToDevice, st));
-        if (!a.fresh) {
-            RASP_CUDA(cudaMemcpyAsync(out->status, in->status, size_t(d), cudaMemcpyDeviceToDevice, st));
-            RASP_CUDA(cudaMemcpyAsync(out->steps, in->steps, size_t(d) * 8, cudaMemcpyDeviceToDevice, st));
-            RASP_CUDA(cudaMemcpyAsync(out->tau_h, in->tau_h, size_t(d) * 8, cudaMemcpyDeviceToDevice, st));
+        int rc2 = dev_copy(out->u, in->u, ub, dv, st);
+        if (!rc2) rc2 = dev_copy(out->y, in->y, yb, dv, st);
+        if (!rc2 && !a.fresh) {
+            rc2 = dev_copy(out->status, in->status, size_t(d), dv, st);
+            if (!rc2) rc2 = dev_copy(out->steps, in->steps, size_t(d) * 8, dv, st);
+            if (!rc2) rc2 = dev_copy(out->tau_h, in->tau_h, size_t(d) * 8, dv, st);
         }
+        if (rc2) return rc2;
     }
-
     if (p->w <= 16) {
         switch (wb) {
         case 1: return dispatch_flags<uint8_t, uint16_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);

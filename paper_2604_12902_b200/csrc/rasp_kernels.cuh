@@ -32,8 +32,6 @@ namespace rasp {
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int8_t kRunning = 0, kHalted = 1, kExhausted = 2;
-constexpr uint32_t kNoVerdict = 0xffffffffu;
-constexpr uint32_t kExhaustBit = 0x80000000u;
 
 // Word arithmetic regime: w == 1 (generic fixedness test), 2 <= w < bits(CT)
 // (masked), w == bits(CT) (native wrap-around, no masks).
@@ -86,6 +84,8 @@ struct EpochArgs {
     uint32_t fresh;                // status=0, steps=0, tau_h=-1 on input
     uint32_t inplace;              // in == out
     uint32_t tile_rows;            // n + ell + 1 + s
+    uint32_t one, two;             // the constants 1 and 2 (see Opq)
+    uint32_t row;                  // bytes per tile row (32 * sizeof(SC))
 };
 
 template <class CT, Arith AR>
@@ -199,11 +199,18 @@ __device__ __forceinline__ void copy_cells(S *__restrict__ dst, const S *__restr
 
 template <class CT>
 struct LaneState {
-    CT i, a;
+    CT i, a;          // i may carry bits above w when RAWI (reduced at every use)
     uint32_t ua, ya;  // addresses of u[u0+1] and y[y0+1]
     uint32_t rem;     // remaining budget at epoch start (clamped)
-    uint32_t tfin;    // verdict time within the epoch (| kExhaustBit), or kNoVerdict
+    uint32_t tlast;   // last local time at which the lane was still live
     bool active;
+};
+
+// Runtime constants held in registers.  Adding a register (rather than an
+// immediate) lets ptxas issue the add on the FMA pipe (IMAD.IADD) instead of
+// the ALU pipe, which the predicate logic of the step already saturates.
+struct Opq {
+    uint32_t one, two, row;
 };
 
 // Cell access.  SMEM kernels address the warp tile with 32-bit shared-window
@@ -247,75 +254,113 @@ __device__ __forceinline__ void st_cell(char *base, uint32_t a, CT v)
     }
 }
 
-// Evaluate the step at local time t and, when allowed, commit it.
-// Fixedness (hv:115): the next configuration equals the current one.  For
-// w >= 2, (i+2) mod 2^w != i, so every advancing case moves i and the test
-// reduces to: opcode not in 1..7, RD with the cursor at capacity, or BNZ
-// taken to its own address.  BUDGET: check t == rem inside the loop (runs
-// whose machines did not all start at the same step count); the final,
-// non-applying evaluation at t == K always checks it.
-template <class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
-__device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
-                                          uint32_t yend, const Geo &g, uint32_t t, bool can_apply)
+// RAWI: power-of-two n and w >= 2 -- i is advanced without masking; every
+// use reduces it ((i mod 2^w) mod n == i & (mask & (n-1)) for n a power of
+// two; equality with a word compares the low w bits).
+template <bool POW2, Arith AR>
+constexpr bool kRawI = POW2 && AR != Arith::W1;
+
+// One fetch/decode of the lane's current instruction: everything the step
+// and the fixedness test need.
+template <class CT>
+struct Fetch {
+    CT o, jw, mj, ud;
+    uint32_t jo;   // address of M[jw mod n]
+};
+
+template <class SC, class CT, bool POW2, Arith AR, bool SMEM>
+__device__ __forceinline__ Fetch<CT> fetch(const LaneState<CT> &L, char *base, uint32_t lm,
+                                           const Geo &g, const Opq &q)
 {
     constexpr uint32_t SH = sizeof(SC) == 2 ? 6 : sizeof(SC) == 4 ? 7 : 8;   // log2(row bytes)
-    constexpr uint32_t ROW = 1u << SH;
     const CT mask = static_cast<CT>(g.mask);
     uint32_t ia, ib;
     if constexpr (POW2) {
-        ia = static_cast<uint32_t>(L.i) & g.nm1;
-        ib = static_cast<uint32_t>(L.i + 1) & g.jm;
+        ia = static_cast<uint32_t>(L.i) & g.jm;
+        ib = static_cast<uint32_t>(L.i + static_cast<CT>(q.one)) & g.jm;
     } else {
         ia = modn<CT, POW2>(L.i, g);
         ib = modn<CT, POW2>(wrap<CT, AR>(L.i + 1, mask), g);
     }
-    const CT o = ld_cell<SC, CT, SMEM>(base, (ia << SH) + lm);
-    const CT jw = ld_cell<SC, CT, SMEM>(base, (ib << SH) + lm);
-    const uint32_t jo = (modn<CT, POW2>(jw, g) << SH) + lm;
-    const CT mj = ld_cell<SC, CT, SMEM>(base, jo);
-    const CT ud = ld_cell<SC, CT, SMEM>(base, L.ua);
-    const CT a0 = L.a;
+    Fetch<CT> f;
+    f.o = ld_cell<SC, CT, SMEM>(base, (ia << SH) + lm);
+    f.jw = ld_cell<SC, CT, SMEM>(base, (ib << SH) + lm);
+    f.jo = (modn<CT, POW2>(f.jw, g) << SH) + lm;
+    f.mj = ld_cell<SC, CT, SMEM>(base, f.jo);
+    f.ud = ld_cell<SC, CT, SMEM>(base, L.ua);
+    return f;
+}
 
-    const bool e6 = (o == 6);
-    const bool rd = e6 & (L.ua < uend);
-    const bool taken = (o == 5) & (a0 != 0);
-    const bool pri = (o == 7) & (L.ya < yend);
-    const CT i2 = wrap<CT, AR>(L.i + 2, mask);
-    bool fixed;
+// Fixedness (hv:115): the next configuration equals the current one.  For
+// w >= 2, (i+2) mod 2^w != i, so every advancing case moves i and the test
+// reduces to: opcode not in 1..7, RD with the cursor at capacity, or BNZ
+// taken to its own address.  For w = 1 the full five-candidate equality.
+template <class CT, bool POW2, Arith AR>
+__device__ __forceinline__ bool is_fixed(const LaneState<CT> &L, const Fetch<CT> &f, uint32_t uend,
+                                         uint32_t yend, const Geo &g, const Opq &q)
+{
+    const CT mask = static_cast<CT>(g.mask);
+    const bool taken = (f.o == 5) & (L.a != 0);
+    const bool ucap = L.ua >= uend;
     if constexpr (AR != Arith::W1) {
-        fixed = (static_cast<CT>(o - 1) > 6) | (e6 & !rd) | (taken & (jw == L.i));
+        bool self;
+        if constexpr (kRawI<POW2, AR> && AR != Arith::FULL) self = ((L.i ^ f.jw) & mask) == 0;
+        else self = f.jw == L.i;
+        return (static_cast<CT>(f.o - static_cast<CT>(q.one)) > 6) | ((f.o == 6) & ucap) | (taken & self);
     } else {
-        const bool adv = (static_cast<CT>(o - 1) < 4) | ((o == 5) & (a0 == 0)) | rd | (o == 7);
-        const CT nif = taken ? jw : (adv ? i2 : L.i);
-        CT naf = (o == 1) ? jw : a0;
-        naf = (o == 2) ? wrap<CT, AR>(a0 + mj, mask) : naf;
-        naf = (o == 3) ? wrap<CT, AR>(a0 * mj, mask) : naf;
-        const CT nmf = (o == 4) ? a0 : (rd ? ud : mj);
-        fixed = (nif == L.i) & (naf == a0) & (nmf == mj) & !rd & !pri;
+        const bool rd = (f.o == 6) & !ucap;
+        const bool pri = (f.o == 7) & (L.ya < yend);
+        const CT i2 = wrap<CT, AR>(L.i + 2, mask);
+        const bool adv = (static_cast<CT>(f.o - 1) < 4) | ((f.o == 5) & (L.a == 0)) | rd | (f.o == 7);
+        const CT ni = taken ? f.jw : (adv ? i2 : L.i);
+        CT na = (f.o == 1) ? f.jw : L.a;
+        na = (f.o == 2) ? wrap<CT, AR>(L.a + f.mj, mask) : na;
+        na = (f.o == 3) ? wrap<CT, AR>(L.a * f.mj, mask) : na;
+        const CT nm = (f.o == 4) ? L.a : (rd ? f.ud : f.mj);
+        return (ni == L.i) & (na == L.a) & (nm == f.mj) & !rd & !pri;
     }
-    if (BUDGET || !can_apply) {
-        const bool fin = L.active & (fixed | (t == L.rem));
-        if (fin) L.tfin = fixed ? t : (t | kExhaustBit);
-        L.active = L.active & !fin;
-    } else {
-        if (L.active & fixed) L.tfin = t;
-        L.active = L.active & !fixed;
-    }
+}
+
+// Evaluate the step at local time t and, when allowed, commit it.
+// BUDGET: check t == rem inside the loop (runs whose machines did not all
+// start at the same step count); the final, non-applying evaluation at
+// t == K always checks it.  A lane's verdict time is the last t at which it
+// was live (tlast); whether it halted or ran out of budget is decided at
+// write-back.
+template <class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
+__device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
+                                          uint32_t yend, const Geo &g, const Opq &q, uint32_t t,
+                                          bool can_apply)
+{
+    const CT mask = static_cast<CT>(g.mask);
+    const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, base, lm, g, q);
+    const CT a0 = L.a;
+    const bool fixed = is_fixed<CT, POW2, AR>(L, f, uend, yend, g, q);
+    if (L.active) L.tlast = t;
+    if (BUDGET || !can_apply) L.active = L.active & !(fixed | (t == L.rem));
+    else L.active = L.active & !fixed;
     const bool app = L.active & can_apply;
     // commit: every update is a predicated move/store keyed on its own case
-    if (app & (o == 1)) L.a = jw;
-    if (app & (o == 2)) L.a = wrap<CT, AR>(a0 + mj, mask);
-    if (app & (o == 3)) L.a = wrap<CT, AR>(a0 * mj, mask);
-    if (app & (o == 4)) st_cell<SC, CT, SMEM>(base, jo, a0);
+    if (app & (f.o == 1)) L.a = f.jw;
+    if (app & (f.o == 2)) L.a = wrap<CT, AR>(a0 + f.mj, mask);
+    if (app & (f.o == 3)) L.a = wrap<CT, AR>(a0 * f.mj, mask);
+    if (app & (f.o == 4)) st_cell<SC, CT, SMEM>(base, f.jo, a0);
+    const bool rd = (f.o == 6) & (L.ua < uend);
     if (app & rd) {
-        st_cell<SC, CT, SMEM>(base, jo, ud);
-        L.ua += ROW;
+        st_cell<SC, CT, SMEM>(base, f.jo, f.ud);
+        L.ua += q.row;
     }
-    if (app & pri) {
-        st_cell<SC, CT, SMEM>(base, L.ya, mj);
-        L.ya += ROW;
+    if (app & (f.o == 7) & (L.ya < yend)) {
+        st_cell<SC, CT, SMEM>(base, L.ya, f.mj);
+        L.ya += q.row;
     }
-    if (app) L.i = taken ? jw : i2;
+    if (app) {
+        const bool taken = (f.o == 5) & (a0 != 0);
+        CT i2;
+        if constexpr (kRawI<POW2, AR>) i2 = L.i + static_cast<CT>(q.two);
+        else i2 = wrap<CT, AR>(L.i + 2, mask);
+        L.i = taken ? f.jw : i2;
+    }
 }
 
 template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
@@ -340,6 +385,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
              (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * static_cast<size_t>(tile_bytes);
         lm = lane * static_cast<uint32_t>(sizeof(SC));
     }
+    const Opq q = {A.one, A.two, A.row};
     const uint32_t U = n * ROW + lm;                       // u[1] of this lane
     const uint32_t Y = (n + A.g.ell + 1) * ROW + lm;       // y[1] of this lane (epoch scratch)
     // generic base for the (cold) row copies: gb + address = generic pointer
@@ -353,6 +399,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     const uint32_t K = A.first ? A.K0 : sc->K[e];
     const int64_t covered = A.first ? 0 : sc->covered[e];
     const uint32_t ntiles = (K == 0 && !A.first) ? 0 : (count + 31) / 32;
+    if (ntiles == 0) return;   // schedule finished: K[e+1] stays 0 from the memset
     const bool copy_side = A.first && !A.inplace;
     const bool fresh = A.fresh != 0;
 
@@ -390,7 +437,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 static_cast<S *>(dst.ac)[id] = static_cast<const S *>(A.in.ac)[id];
                 copy_cells(static_cast<S *>(dst.M) + id * n, srcM, n);
             }
-            L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tfin = kNoVerdict;
+            L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tlast = 0;
             if (running) {
                 L.i = static_cast<CT>(static_cast<const S *>(src.iw)[id]);
                 L.a = static_cast<CT>(static_cast<const S *>(src.ac)[id]);
@@ -413,16 +460,16 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             uint32_t t = 0;
             bool live = __any_sync(kFull, L.active);
             for (; live && t + 2 <= K; t += 2) {
-                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t, true);
-                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t + 1, true);
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, q, t, true);
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, q, t + 1, true);
                 live = __any_sync(kFull, L.active);
             }
             if (live && t < K) {
-                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, t, true);
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, q, t, true);
                 ++t;
                 live = __any_sync(kFull, L.active);
             }
-            if (live) rasp_step<SC, CT, POW2, AR, true, SMEM>(L, tb, lm, uend, yend, g, K, false);
+            if (live) rasp_step<SC, CT, POW2, AR, true, SMEM>(L, tb, lm, uend, yend, g, q, K, false);
         }
         if (lane == 0) next = atomicAdd(&sc->tile_ctr[e], 1u);   // overlaps the write-back
 
@@ -439,6 +486,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const uint32_t y0_start = static_cast<uint32_t>(static_cast<const S *>(src.y)[id * ycols]);
             const uint32_t u0 = (L.ua - U) / ROW;
             const uint32_t y0 = (L.ya - Y) / ROW;
+            if constexpr (kRawI<POW2, AR>) L.i &= static_cast<CT>(A.g.mask);
             S *dY = static_cast<S *>(dst.y) + id * ycols;
             const SC *colY = reinterpret_cast<const SC *>(gb + Y);
             for (uint32_t k = y0_start; k < y0; ++k) dY[k + 1] = static_cast<S>(colY[k * 32]);
@@ -446,11 +494,18 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             static_cast<S *>(dst.iw)[id] = static_cast<S>(L.i);
             static_cast<S *>(dst.ac)[id] = static_cast<S>(L.a);
             static_cast<S *>(dst.u)[id * ucols] = static_cast<S>(u0);
-            store_row<S, SC>(static_cast<S *>(dst.M) + id * n, n, reinterpret_cast<const SC *>(gb + lm));
-            if (L.tfin != kNoVerdict) {
-                const int64_t tend = steps0 + (L.tfin & ~kExhaustBit);
+            if (!L.active) {
+                // verdict at tlast: halted, unless the budget ran out there and
+                // the configuration is not a fixed point
+                bool halted = true;
+                if (L.tlast == L.rem) {
+                    const uint32_t uend = U + A.g.ell * ROW, yend = Y + A.g.s * ROW;
+                    const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, tb, lm, A.g, q);
+                    halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, A.g, q);
+                }
+                const int64_t tend = steps0 + L.tlast;
                 dst.steps[id] = tend;
-                if (L.tfin & kExhaustBit) {
+                if (!halted) {
                     dst.status[id] = kExhausted;
                     if (fresh) dst.tau_h[id] = -1;
                 } else {
@@ -462,6 +517,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 sid = static_cast<uint32_t>(id);
                 if (!fresh) dst.steps[id] = steps0 + K;
             }
+            store_row<S, SC>(static_cast<S *>(dst.M) + id * n, n, reinterpret_cast<const SC *>(gb + lm));
         }
         const unsigned sv = __ballot_sync(kFull, survivor);
         if (sv) {
@@ -497,6 +553,18 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             }
         }
     }
+}
+
+// Bulk device copy on the SMs (keeps the copy engines free for host traffic).
+__global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ dst, uint64_t n16,
+                            const unsigned char *__restrict__ srcb, unsigned char *__restrict__ dstb,
+                            uint64_t tail)
+{
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n16; k += stride)
+        dst[k] = src[k];
+    if (blockIdx.x == 0)
+        for (uint64_t k = threadIdx.x; k < tail; k += blockDim.x) dstb[k] = srcb[k];
 }
 
 // 102-bucket halting histogram (hypervisor.py:326-352).

@@ -25,8 +25,8 @@ class HostPipeline:
         self.device = torch.device(device) if device is not None else torch.device("cuda")
         self.engine = engine or get_engine(params, self.device)
         self.wb = word_bytes or params.dtype.itemsize
-        self.src = DeviceBatch.empty(d, params, self.device, self.wb, fresh=True)
-        self.dst = DeviceBatch.empty(d, params, self.device, self.wb, fresh=False)
+        # one device batch: each chunk is copied in, run in place, copied out
+        self.dev = DeviceBatch.empty(d, params, self.device, self.wb, fresh=False)
         self.chunks = max(1, min(chunks, (d + 4095) // 4096))
         step = (d + self.chunks - 1) // self.chunks
         self.bounds = [(a, min(d, a + step)) for a in range(0, d, step)] if d else []
@@ -74,18 +74,18 @@ class HostPipeline:
         for a, b in self.bounds:
             with torch.cuda.stream(self.s_in):
                 for k in WORD_FIELDS:
-                    getattr(self.src, k)[a:b].copy_(pinned[k][a:b], non_blocking=True)
+                    getattr(self.dev, k)[a:b].copy_(pinned[k][a:b], non_blocking=True)
                 ev_in = torch.cuda.Event()
                 ev_in.record(self.s_in)
             self.s_run.wait_event(ev_in)
-            self.engine.run(self._view(self.src, a, b), tau_max, epoch,
-                            out=self._view(self.dst, a, b), fresh=True, stream=self.s_run)
+            # fresh c0: status/steps/tau_h are outputs only, never read
+            self.engine.run(self._view(self.dev, a, b), tau_max, epoch, fresh=True, stream=self.s_run)
             ev_run = torch.cuda.Event()
             ev_run.record(self.s_run)
             self.s_out.wait_event(ev_run)
             with torch.cuda.stream(self.s_out):
                 for k in ALL_FIELDS:
-                    self.host_out[k][a:b].copy_(getattr(self.dst, k)[a:b], non_blocking=True)
+                    self.host_out[k][a:b].copy_(getattr(self.dev, k)[a:b], non_blocking=True)
         main.wait_stream(self.s_out)
         e1.record(main)
         e1.synchronize()
