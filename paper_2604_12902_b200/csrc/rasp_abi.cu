@@ -128,11 +128,19 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
     auto kern = rasp::epoch_kernel<S, SC, CT, POW2, AR, BUDGET, SMEM>;
     const int threads = 32 * pl.warps_per_block;
     if (SMEM) {
-        RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.dyn_smem)));
-        int per_sm = 0;
-        RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, pl.dyn_smem));
-        if (per_sm < 1) return RASP_ECAPACITY;
-        pl.blocks = per_sm * dv.nsm;
+        // attribute + occupancy per (instantiation, device, smem size), queried once
+        struct Cached { int dev = -1; size_t smem = 0; int per_sm = 0; };
+        static thread_local Cached c;
+        if (c.dev != dv.id || c.smem != pl.dyn_smem) {
+            RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.dyn_smem)));
+            int per_sm = 0;
+            RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, pl.dyn_smem));
+            c.dev = dv.id;
+            c.smem = pl.dyn_smem;
+            c.per_sm = per_sm;
+        }
+        if (c.per_sm < 1) return RASP_ECAPACITY;
+        pl.blocks = c.per_sm * dv.nsm;
     }
     const uint64_t tiles = (d + 31) / 32;
     const uint64_t need_blocks = (tiles + pl.warps_per_block - 1) / pl.warps_per_block;
@@ -143,6 +151,7 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
     // only finish sooner (it lengthens epochs once survivors stop halting).
     const uint64_t K0 = uint64_t(std::min<int64_t>(std::max<int64_t>(epoch, 1), tau_max));
     int planned = 1;
+    bool covers = int64_t(K0) >= tau_max;
     {
         uint64_t cov = K0, k = std::max<uint64_t>(K0, 1);
         while (int64_t(cov) < tau_max && planned < kPollAfter) {
@@ -150,9 +159,11 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
             cov += k;
             ++planned;
         }
+        covers = int64_t(cov) >= tau_max;
     }
     for (int e = 0;; ++e) {
         if (e >= kMaxEpochs) return RASP_ECAPACITY;
+        if (e >= planned && covers) break;   // fully asynchronous in the common case
         if (e >= planned) {
             // long budgets: ask the device whether another epoch is needed
             uint32_t knext = 0;
