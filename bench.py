@@ -4,8 +4,12 @@
 
 Workload (BASELINE.json configs[1]): per GPU, 2^20 synthetic
 programs from generator G (seed = rank), w=16, n=64, ell=8, s=8, run to halt
-with a 1024-step cap.  Each rank runs its own shard (weak scaling; the only
-collective is the all-reduce of the 102-bucket halting histogram).
+with a 1024-step cap.  Each rank runs its own shard (weak scaling; no
+collective on the data path -- after the run the 102-bucket halting
+histogram is all-reduced and rank 0 gathers every shard's verdicts and
+output tapes over NCCL).  --config c3 is BASELINE configs[2]: 16M machines in
+total split across the ranks (strong scaling); c1 and c5 are configs[0] and
+configs[4].
 
 One "step" = one full run of the batch from c0 (out-of-place, c0 is never
 modified) plus the on-device halting histogram.  Metric: machine-steps/s
@@ -157,6 +161,9 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     d, w, n, ell, s, tau, desc = CONFIGS[args.config]
+    strong = args.config == "c3"        # 16M machines in total, split across the ranks
+    if strong and args.impl != "reference":
+        d = -(-d // world)
     metric = "machine-steps/s"
 
     if args.impl == "reference":
@@ -202,11 +209,19 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
     stream = torch.cuda.current_stream(dev)
 
+    # N > 1: rank 0 gathers every shard's verdicts and output tapes
+    gathers = []
+    if world > 1:
+        for t in (dst.status, dst.steps, dst.tau_h, dst.y.view(torch.uint8)):
+            gathers.append((t, [torch.empty_like(t) for _ in range(world)] if rank == 0 else None))
+
     def one_step():
         eng.run(src, tau, args.epoch, out=dst, fresh=True, stream=stream)
         eng.histogram(dst, out=hist, stream=stream)
         if world > 1:
             dist.all_reduce(hist)
+            for t, parts in gathers:
+                dist.gather(t, parts, dst=0)
 
     for _ in range(max(args.warmup, 0)):
         one_step()
@@ -302,13 +317,15 @@ def main():
     line = {
         "metric": metric, "value": value, "unit": "machine-steps/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u16" if w <= 16 else "u32",
+        "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+        "dtype": "u16" if w <= 16 else "u32",
         "data": "synthetic (generator G, SURVEY §8d; seed = rank)",
         "config": {"workload": args.config, "desc": desc, "d_per_gpu": d, "w": w, "n": n,
                    "ell": ell, "s": s, "tau_max": tau, "epoch": args.epoch,
                    "machine_steps_per_gpu": machine_steps, "halted_frac": total_halted / (d * world),
                    "l2": "flushed between steps (256 MB write, outside the events)",
-                   "parallelism": f"shard{world}" if world > 1 else "1 GPU"},
+                   "parallelism": (f"{world} contiguous shards, NCCL all-reduce(histogram) + gather(verdicts, y)"
+                                   if world > 1 else "1 GPU")},
         "programs_per_s": d * world / t_step,
         "e2e": {"value": total_steps / t_e2e, "unit": "machine-steps/s",
                 "h2d_bytes_per_step": pipe.h2d_bytes, "d2h_bytes_per_step": pipe.d2h_bytes,
