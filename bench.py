@@ -47,6 +47,10 @@ CONFIGS = {
            "16M random programs/GPU, w=16 n=64 l=8 s=8, run to halt (cap 1024)"),
     "c5": (1 << 20, 32, 256, 32, 32, 1024,
            "1M random programs/GPU, w=32 n=256 l=32 s=32, divergent halting (cap 1024)"),
+    # d = programs; machines = programs x 2^w inputs (SURVEY §8d C4 domain)
+    "c4": (1 << 28, 8, 16, 1, 1, 64,
+           "exhaustive: all 2^28 programs of m=4 pairs (3-bit opcode, 4-bit operand), w=8 n=16, "
+           "x all 256 inputs, tau 64, per-program records"),
 }
 N_ALG_INSTR = 40   # algorithmic integer issues per machine-step
 
@@ -125,12 +129,27 @@ def cpu_reference(cfg_name, steps_k, warmup, sample_d=None, seed=0):
     from paper_2604_12902_b200.machine import MachineParams
     from paper_2604_12902_b200.workload import synthetic_c0
     d, w, n, ell, s, tau, _ = CONFIGS[cfg_name]
-    sample = min(d, sample_d or (1 << 16))
-    p = MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
-    c0 = synthetic_c0(sample, p, seed=seed)
     cores = len(os.sched_getaffinity(0))
     oracle.load()
     times, steps_total = [], 0
+    if cfg_name == "c4":
+        from paper_2604_12902_b200.enumeration import C4
+        sample = min(d, (sample_d or (1 << 16)) // 4)
+        for it in range(warmup + steps_k):
+            t0 = time.perf_counter()
+            _, steps_total = oracle.enumerate_records(C4.m, C4.opcode_bits, C4.operand_bits, C4.w,
+                                                      C4.n, C4.tau_max, 0, sample, threads=cores)
+            dt = time.perf_counter() - t0
+            if it >= warmup:
+                times.append(dt)
+        best = min(times) if times else float("nan")
+        return {"value": steps_total / best, "unit": "machine-steps/s", "cores": cores,
+                "kind": "port", "sample": f"programs [0, {sample}) of the C4 domain x 256 inputs, "
+                f"{steps_total} machine-steps, {cores} threads, best of {len(times)}",
+                "seconds": best}
+    sample = min(d, sample_d or (1 << 16))
+    p = MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
+    c0 = synthetic_c0(sample, p, seed=seed)
     for it in range(warmup + steps_k):
         t0 = time.perf_counter()
         out = oracle.worker_arrays(c0, w, n, ell, s, tau, epoch=64, workers=cores)
@@ -143,6 +162,95 @@ def cpu_reference(cfg_name, steps_k, warmup, sample_d=None, seed=0):
             "kind": "port", "sample": f"{sample} machines of {cfg_name} (generator G seed {seed}), "
             f"{steps_total} machine-steps, _worker semantics, W={cores} threads, q=64, "
             f"best of {len(times)}", "seconds": best}
+
+
+def bench_enumeration(args, world, rank, dev, desc):
+    """BASELINE config 4: one step = the whole 2^28-program domain (sharded by
+    contiguous rank ranges across GPUs), records left in HBM; e2e adds the
+    D2H of every record."""
+    import torch
+    import torch.distributed as dist
+    from paper_2604_12902_b200 import _native
+    from paper_2604_12902_b200.enumeration import C4, enumerate_device
+    from paper_2604_12902_b200.sharding import shard_bounds
+    lib = _native.load()
+    lo, hi = shard_bounds(C4.programs, world, rank)
+    cnt = hi - lo
+    rec = torch.empty(cnt, dtype=torch.uint64, device=dev)
+    st = torch.zeros(1, dtype=torch.uint64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(max(args.warmup, 1)):
+        st.zero_()
+        enumerate_device(C4, lo, cnt, rec, st)
+    torch.cuda.synchronize()
+    steps = int(st.cpu().numpy()[0])
+    allh = int((rec.view(torch.int64) < 0).sum().item())     # bit 63: halted on every input
+    clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clocks.start()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = lib.rasp_launch_count()
+    ts = []
+    for _ in range(args.steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        enumerate_device(C4, lo, cnt, rec, st)
+        e1.record(stream)
+        ts.append((e0, e1))
+    torch.cuda.synchronize()
+    launches = lib.rasp_launch_count() - l0
+    clk = clocks.stop()
+    t_step = statistics.mean(a.elapsed_time(b) / 1e3 for a, b in ts)
+    # e2e: run + copy every record to pinned host memory
+    host = torch.empty(cnt, dtype=torch.uint64, pin_memory=True)
+    te = []
+    for _ in range(max(2, min(args.steps, 5))):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        enumerate_device(C4, lo, cnt, rec, st)
+        host.copy_(rec, non_blocking=True)
+        e1.record(stream)
+        e1.synchronize()
+        te.append(e0.elapsed_time(e1) / 1e3)
+    t_e2e = statistics.mean(te)
+    tot = torch.tensor([t_step, t_e2e], dtype=torch.float64, device=dev)
+    agg = torch.tensor([steps, allh, cnt], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(tot, op=dist.ReduceOp.MAX)
+        dist.all_reduce(agg)
+    t_step, t_e2e = (float(v) for v in tot.tolist())
+    steps_all, allh_all, progs = (int(v) for v in agg.tolist())
+    if rank == 0:
+        _, sm_mhz, peak_kind = _peaks()
+        issue_peak = 148 * 4 * 32 * sm_mhz * 1e6
+        ach = steps * N_ALG_INSTR / t_step
+        line = {
+            "metric": "machine-steps/s", "value": steps_all / t_step, "unit": "machine-steps/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u8",
+            "data": "exhaustive (every program of the domain x every input, decoded on device)",
+            "config": {"workload": "c4", "desc": desc, "programs": progs, "machines": progs * 256,
+                       "machine_steps": steps_all, "all_halting_programs": allh_all,
+                       "parallelism": f"{world} contiguous rank shards" if world > 1 else "1 GPU"},
+            "programs_per_s": progs / t_step,
+            "e2e": {"value": steps_all / t_e2e, "unit": "machine-steps/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": cnt * 8, "ms_per_step": t_e2e * 1e3},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "issue", "unit": "Tinstr/s", "achieved": ach / 1e12,
+                         "peak": issue_peak / 1e12, "frac": ach / issue_peak, "traffic": None,
+                         "per_unit": f"{N_ALG_INSTR} int-instr per machine-step (SURVEY §8d); "
+                                     "decode and reduction are extra work not credited"},
+            "clocks": clk,
+        }
+        if not args.no_cpu_baseline and world == 1:
+            cb = cpu_reference("c4", 1, 0, args.cpu_sample)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
 
 
 def main():
@@ -161,8 +269,8 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     d, w, n, ell, s, tau, desc = CONFIGS[args.config]
-    strong = args.config == "c3"        # 16M machines in total, split across the ranks
-    if strong and args.impl != "reference":
+    strong = args.config in ("c3", "c4")   # fixed total work, split across the ranks
+    if args.config == "c3" and args.impl != "reference":
         d = -(-d // world)
     metric = "machine-steps/s"
 
@@ -174,8 +282,10 @@ def main():
         line = {
             "metric": metric, "value": cb["value"], "unit": "machine-steps/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "u64", "data": "synthetic (generator G)",
+            "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
+            "vs_baseline": None, "dtype": "u64",
+            "data": "exhaustive enumeration" if args.config == "c4" else "synthetic (generator G)",
             "config": {"workload": args.config, "desc": desc, "w": w, "n": n, "ell": ell, "s": s,
                        "tau_max": tau, "d_sample": min(d, args.cpu_sample)},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -192,6 +302,9 @@ def main():
     dev = torch.device("cuda", local_rank)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
+
+    if args.config == "c4":
+        return bench_enumeration(args, world, rank, dev, desc)
 
     from paper_2604_12902_b200 import _native
     from paper_2604_12902_b200.engine import DeviceBatch

@@ -95,6 +95,28 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out,
              int64_t tau_max, int64_t epoch, uint32_t flags,
              void *workspace, size_t workspace_bytes, void *stream);
 
+/* Exhaustive program enumeration (BASELINE config 4).
+ * Program rank r: pair k = bits [k*(ob+pb), (k+1)*(ob+pb)) of r, opcode = the
+ * low ob bits, operand = the next pb bits.  Machine (r, x) is
+ * init_config(P_r, [x]) (machine.py:289-309) with ell = s = 1, for every
+ * input word x in [0, 2^w), run for at most tau_max steps.  Per program, one
+ * record: bit 63 = every input reached a fixed point within tau_max; bits
+ * 0..62 = sum over x of mix64(x | halted<<8 | y0<<9 | y1<<10 | tau_h<<18)
+ * (splitmix64 finaliser; y1 and tau_h count only when written / halted).
+ * records: uint64[count] device buffer; steps_total: device counter that
+ * accumulates the applied machine-steps.  2 <= w <= 8. */
+typedef struct rasp_enum_params {
+    uint32_t m;             /* instruction pairs */
+    uint32_t opcode_bits;   /* ob */
+    uint32_t operand_bits;  /* pb */
+    uint32_t w;             /* word width, 2..8 */
+    uint32_t n;             /* memory cells, >= 2m */
+    uint32_t tau_max;
+} rasp_enum_params;
+
+int rasp_enumerate(const rasp_enum_params *p, uint64_t first_rank, uint64_t count,
+                   uint64_t *records, unsigned long long *steps_total, void *stream);
+
 /* Bucketed halting-time histogram (hypervisor.py:326-352): out[0..99] exact
  * tau_h, out[100] tau_h >= 100, out[101] EXHAUSTED count.  out: int64[102]
  * device buffer, overwritten. */

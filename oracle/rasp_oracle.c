@@ -183,3 +183,87 @@ int oracle_step(u64 *i, u64 *a, u64 *M, u64 *u, u64 *y,
     oracle_state st = {i, a, M, u, y, &status, &steps, &tau, 1, wmask, n, ell, s};
     return oracle_advance(&st, 0, 1);
 }
+
+/* ---- exhaustive enumeration (BASELINE config 4) -------------------------------
+ * Same machine semantics (oracle_advance) driven per (program rank, input x),
+ * run_to_fixpoint style (machine.py:336-357) with budget tau; the per-program
+ * record definition mirrors include/raspvisor_b200.h (rasp_enumerate). */
+static uint64_t mix64(uint64_t z)
+{
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+typedef struct {
+    u64 m, ob, pb, w, n, tau, first, count;
+    u64 *records;
+    u64 steps;
+    i64 g, W;
+} enum_arg;
+
+static void *enum_main(void *p)
+{
+    enum_arg *a = (enum_arg *)p;
+    const u64 n = a->n, mask = (a->w == 64) ? ~0ull : ((1ull << a->w) - 1);
+    const u64 pw = a->ob + a->pb;
+    u64 *M = (u64 *)calloc(n, sizeof(u64));
+    u64 iw, ac, u[2], y[2];
+    int8_t st;
+    i64 steps, tau_h;
+    oracle_state s = {&iw, &ac, M, u, y, &st, &steps, &tau_h, 1, mask, n, 1, 1};
+    a->steps = 0;
+    for (u64 pi = (u64)a->g; pi < a->count; pi += (u64)a->W) {
+        const u64 r = a->first + pi;
+        u64 sum = 0;
+        int all = 1;
+        for (u64 x = 0; x <= mask && x < 256; ++x) {
+            memset(M, 0, n * sizeof(u64));
+            for (u64 k = 0; k < a->m && 2 * k + 1 < n; ++k) {
+                const u64 pair = (r >> (k * pw)) & ((1ull << pw) - 1);
+                M[2 * k] = pair & ((1ull << a->ob) - 1);
+                M[2 * k + 1] = pair >> a->ob;
+            }
+            iw = 0; ac = 0; u[0] = 0; u[1] = x; y[0] = 0; y[1] = 0;
+            u64 t = 0;
+            int halted = 0;
+            for (;;) {                           /* run_to_fixpoint, m:345-357 */
+                if (oracle_advance(&s, 0, 0)) { halted = 1; break; }
+                if (t == a->tau) break;
+                oracle_advance(&s, 0, 1);
+                ++t;
+            }
+            a->steps += t;
+            if (!halted) all = 0;
+            const u64 key = x | ((u64)halted << 8) | (y[0] << 9) | ((y[0] ? y[1] : 0) << 10) |
+                            ((u64)(halted ? t : 0) << 18);
+            sum += mix64(key);
+        }
+        a->records[pi] = ((u64)all << 63) | (sum & 0x7fffffffffffffffull);
+    }
+    free(M);
+    return NULL;
+}
+
+/* records[count]; returns the applied machine-steps. */
+u64 oracle_enumerate(u64 m, u64 ob, u64 pb, u64 w, u64 n, u64 tau, u64 first, u64 count,
+                     u64 *records, i64 threads)
+{
+    if (threads < 1) threads = 1;
+    enum_arg *args = (enum_arg *)calloc((size_t)threads, sizeof(enum_arg));
+    pthread_t *th = (pthread_t *)calloc((size_t)threads, sizeof(pthread_t));
+    for (i64 g = 0; g < threads; ++g) {
+        args[g] = (enum_arg){m, ob, pb, w, n, tau, first, count, records, 0, g, threads};
+        if (threads > 1) pthread_create(&th[g], NULL, enum_main, &args[g]);
+        else enum_main(&args[g]);
+    }
+    u64 total = 0;
+    for (i64 g = 0; g < threads; ++g) {
+        if (threads > 1) pthread_join(th[g], NULL);
+        total += args[g].steps;
+    }
+    free(args);
+    free(th);
+    return total;
+}

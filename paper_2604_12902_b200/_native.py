@@ -22,12 +22,18 @@ RASP_FRESH = 1
 # symbols declared by include/raspvisor_b200.h
 EXPORTS = ("rasp_workspace_bytes", "rasp_run", "rasp_histogram", "rasp_validate",
            "rasp_error_string", "rasp_last_cuda_error", "rasp_abi_version",
-           "rasp_launch_count")
+           "rasp_launch_count", "rasp_enumerate")
 
 
 class RaspParams(ctypes.Structure):
     _fields_ = [("w", ctypes.c_uint32), ("n", ctypes.c_uint32),
                 ("ell", ctypes.c_uint64), ("s", ctypes.c_uint64)]
+
+
+class RaspEnumParams(ctypes.Structure):
+    _fields_ = [("m", ctypes.c_uint32), ("opcode_bits", ctypes.c_uint32),
+                ("operand_bits", ctypes.c_uint32), ("w", ctypes.c_uint32),
+                ("n", ctypes.c_uint32), ("tau_max", ctypes.c_uint32)]
 
 
 class RaspBatch(ctypes.Structure):
@@ -72,6 +78,8 @@ def load():
     lib.rasp_last_cuda_error.restype = ctypes.c_char_p
     lib.rasp_abi_version.argtypes = []
     lib.rasp_abi_version.restype = ctypes.c_int
+    lib.rasp_enumerate.argtypes = [ctypes.POINTER(RaspEnumParams), U64, U64, P, P, P]
+    lib.rasp_enumerate.restype = ctypes.c_int
     lib.rasp_launch_count.argtypes = []
     lib.rasp_launch_count.restype = ctypes.c_ulonglong
     if lib.rasp_abi_version() != ABI_VERSION:

@@ -347,6 +347,54 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     return dispatch_flags<uint64_t, uint64_t, uint64_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
 }
 
+int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t count, uint64_t *records,
+                   unsigned long long *steps_total, void *stream)
+{
+    if (!ep || !records || !steps_total) return RASP_EPARAM;
+    if (ep->w < 2 || ep->w > 8 || ep->n < 2 || ep->n > 4096 || ep->m < 1 || ep->opcode_bits < 1 ||
+        ep->operand_bits < 1 || ep->opcode_bits > ep->w || ep->operand_bits > ep->w ||
+        uint64_t(ep->m) * (ep->opcode_bits + ep->operand_bits) > 63)
+        return RASP_EPARAM;
+    if (2 * ep->m > ep->n) return RASP_ECAPACITY;
+    if (count == 0) return RASP_OK;
+    Device dv;
+    int rc = device_info(dv);
+    if (rc) return rc;
+    rasp::EnumArgs a;
+    std::memset(&a, 0, sizeof a);
+    a.g.mask = (1ull << ep->w) - 1;
+    a.g.n = ep->n;
+    a.g.nm1 = ep->n - 1;
+    a.g.jm = uint32_t(a.g.mask & uint64_t(ep->n - 1));
+    a.g.fm = ~0ull / ep->n + 1;
+    a.g.ell = 1;
+    a.g.s = 1;
+    a.first = first_rank;
+    a.count = count;
+    a.records = records;
+    a.steps_total = steps_total;
+    a.m = ep->m;
+    a.ob = ep->opcode_bits;
+    a.pb = ep->operand_bits;
+    a.tau = ep->tau_max;
+    a.one = 1;
+    a.two = 2;
+    a.row = 64;
+    const size_t smem = size_t(8) * (ep->n + 3) * 64;
+    const bool pow2 = (ep->n & (ep->n - 1)) == 0;
+    auto kern = pow2 ? rasp::enum_kernel<true, rasp::Arith::NARROW> : rasp::enum_kernel<false, rasp::Arith::NARROW>;
+    RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    int per_sm = 0;
+    RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    if (per_sm < 1) return RASP_ECAPACITY;
+    const uint64_t grid = std::min<uint64_t>(count, uint64_t(per_sm) * dv.nsm * 8);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    kern<<<unsigned(grid), 256, smem, st>>>(a);
+    RASP_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return RASP_OK;
+}
+
 int rasp_histogram(const int8_t *status, const int64_t *tau_h, uint64_t d, int64_t *out, void *stream)
 {
     cudaStream_t st = static_cast<cudaStream_t>(stream);

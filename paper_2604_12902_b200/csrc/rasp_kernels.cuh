@@ -555,6 +555,142 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     }
 }
 
+// --- exhaustive enumeration (BASELINE config 4) -------------------
+//
+// Program rank r in [0, 2^(m*(ob+pb))): pair k occupies bits [k*(ob+pb), ...)
+// of r, opcode = low ob bits, operand = next pb bits.  Machine (r, x) is
+// c0(P_r, (x)) with ell = s = 1 and x in [0, 2^w) (init_config, m:289-309).
+// One block runs one program on all 2^w inputs (w <= 8: 256 lanes), each
+// warp on 32 of them, with the same tile/step code as the batch engine, then
+// reduces the inputs into one 64-bit record:
+//   bit 63     all inputs reached a fixed point within tau_max
+//   bits 0..62 sum over x of mix64(x | halted << 8 | y0 << 9 | y1 << 10 | tau_h << 18)
+// (a sum, so the reduction order cannot change it).
+
+struct EnumArgs {
+    Geo g;
+    uint64_t first;          // first program rank
+    uint64_t count;          // programs
+    uint64_t *records;       // [count]
+    unsigned long long *steps_total;
+    uint32_t m, ob, pb;      // pairs, opcode bits, operand bits
+    uint32_t tau;            // step budget
+    uint32_t one, two, row;
+};
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z)
+{
+    z += 0x9e3779b97f4a7c15ull;
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+template <bool POW2, Arith AR>
+__global__ void __launch_bounds__(256)
+enum_kernel(const EnumArgs A)
+{
+    using SC = uint16_t;
+    using CT = uint32_t;
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    __shared__ unsigned long long red_sum[8];
+    __shared__ unsigned int red_all[8];
+    __shared__ unsigned long long red_steps[8];
+    constexpr uint32_t ROW = 32 * sizeof(SC);
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t wib = threadIdx.x >> 5;
+    const Geo g = A.g;
+    const uint32_t n = g.n;
+    const uint32_t tile_bytes = (n + 3) * ROW;     // M, u[1] + pad, y[1]
+    char *tb = reinterpret_cast<char *>(smem_raw);
+    const uint32_t lm = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes +
+                        lane * static_cast<uint32_t>(sizeof(SC));
+    char *gb = reinterpret_cast<char *>(smem_raw) - static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+    SC *colM = reinterpret_cast<SC *>(gb + lm);
+    const uint32_t U = n * ROW + lm, Y = (n + 2) * ROW + lm;
+    const uint32_t uend = U + ROW, yend = Y + ROW;
+    const Opq q = {A.one, A.two, A.row};
+    const uint32_t pw = A.ob + A.pb;
+    const uint32_t x = threadIdx.x;                 // the input word of this lane
+    const bool valid_x = x <= static_cast<uint32_t>(g.mask);
+
+    for (uint64_t pi = blockIdx.x; pi < A.count; pi += gridDim.x) {
+        const uint64_t r = A.first + pi;
+        // c0: decode the program into M, input x into u[1], empty output
+        for (uint32_t k = 0; k < n; ++k) colM[k * 32] = 0;
+        for (uint32_t k = 0; k < A.m && 2 * k + 1 < n; ++k) {
+            const uint32_t pair = static_cast<uint32_t>(r >> (k * pw)) & ((1u << pw) - 1u);
+            colM[(2 * k) * 32] = static_cast<SC>(pair & ((1u << A.ob) - 1u));
+            colM[(2 * k + 1) * 32] = static_cast<SC>(pair >> A.ob);
+        }
+        *reinterpret_cast<SC *>(gb + U) = static_cast<SC>(x);
+        LaneState<CT> L;
+        L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tlast = 0; L.rem = A.tau;
+        L.active = valid_x;
+        asm volatile("" ::: "memory");
+        const uint32_t K = A.tau;
+        uint32_t t = 0;
+        bool live = __any_sync(kFull, L.active);
+        for (; live && t + 2 <= K; t += 2) {
+            rasp_step<SC, CT, POW2, AR, false, true>(L, tb, lm, uend, yend, g, q, t, true);
+            rasp_step<SC, CT, POW2, AR, false, true>(L, tb, lm, uend, yend, g, q, t + 1, true);
+            live = __any_sync(kFull, L.active);
+        }
+        if (live && t < K) {
+            rasp_step<SC, CT, POW2, AR, false, true>(L, tb, lm, uend, yend, g, q, t, true);
+            ++t;
+            live = __any_sync(kFull, L.active);
+        }
+        if (live) rasp_step<SC, CT, POW2, AR, true, true>(L, tb, lm, uend, yend, g, q, K, false);
+
+        uint64_t v = 0;
+        uint32_t halted = 1;
+        uint64_t my_steps = 0;
+        if (valid_x) {
+            halted = 1;
+            uint32_t tend = L.tlast;
+            if (L.active) {
+                halted = 0;            // cannot happen: the final evaluation classifies everyone
+            } else if (L.tlast == L.rem) {
+                const Fetch<CT> f = fetch<SC, CT, POW2, AR, true>(L, tb, lm, g, q);
+                halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, g, q) ? 1u : 0u;
+            }
+            const uint32_t y0 = (L.ya - Y) / ROW;
+            const uint32_t y1 = *reinterpret_cast<const SC *>(gb + Y);   // y[1] (0 unless written)
+            const uint64_t key = static_cast<uint64_t>(x) | (static_cast<uint64_t>(halted) << 8) |
+                                 (static_cast<uint64_t>(y0) << 9) |
+                                 (static_cast<uint64_t>(y0 ? y1 : 0u) << 10) |
+                                 (static_cast<uint64_t>(halted ? tend : 0u) << 18);
+            v = mix64(key);
+            my_steps = tend;
+        }
+        // block reduction: sum of v, AND of halted, sum of steps
+        for (int off = 16; off; off >>= 1) {
+            v += __shfl_down_sync(kFull, v, off);
+            my_steps += __shfl_down_sync(kFull, my_steps, off);
+        }
+        const unsigned all = __all_sync(kFull, halted != 0);
+        if (lane == 0) {
+            red_sum[wib] = v;
+            red_all[wib] = all;
+            red_steps[wib] = my_steps;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t sum = 0, st = 0;
+            unsigned a = 1;
+            for (uint32_t w2 = 0; w2 < (blockDim.x >> 5); ++w2) {
+                sum += red_sum[w2];
+                a &= red_all[w2];
+                st += red_steps[w2];
+            }
+            A.records[pi] = (static_cast<uint64_t>(a) << 63) | (sum & 0x7fffffffffffffffull);
+            atomicAdd(A.steps_total, static_cast<unsigned long long>(st));
+        }
+        __syncthreads();
+    }
+}
+
 // Bulk device copy on the SMs (keeps the copy engines free for host traffic).
 __global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ dst, uint64_t n16,
                             const unsigned char *__restrict__ srcb, unsigned char *__restrict__ dstb,
