@@ -126,22 +126,38 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
                   uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
 {
     auto kern = rasp::epoch_kernel<S, SC, CT, POW2, AR, BUDGET, SMEM>;
-    const int threads = 32 * pl.warps_per_block;
     if (SMEM) {
-        // attribute + occupancy per (instantiation, device, smem size), queried once
-        struct Cached { int dev = -1; size_t smem = 0; int per_sm = 0; };
+        // warps per block chosen to maximise resident warps per SM (ties: more
+        // warps per block); attribute + occupancy queried once per
+        // (instantiation, device, tile size)
+        struct Cached { int dev = -1; size_t tile = 0; int wpb = 0; int per_sm = 0; };
         static thread_local Cached c;
-        if (c.dev != dv.id || c.smem != pl.dyn_smem) {
-            RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(pl.dyn_smem)));
-            int per_sm = 0;
-            RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, pl.dyn_smem));
+        if (c.dev != dv.id || c.tile != pl.tile_bytes) {
+            int best_w = 0, best_ps = 0;
+            for (int wpb = kWarpsPerBlockMax; wpb >= 1; --wpb) {
+                const size_t smem = pl.tile_bytes * size_t(wpb);
+                if (smem > size_t(dv.smem_optin)) continue;
+                RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                int per_sm = 0;
+                RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
+                if (per_sm * wpb > best_ps * best_w) {
+                    best_w = wpb;
+                    best_ps = per_sm;
+                }
+            }
+            if (best_w == 0) return RASP_ECAPACITY;
+            RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(pl.tile_bytes * size_t(best_w))));
             c.dev = dv.id;
-            c.smem = pl.dyn_smem;
-            c.per_sm = per_sm;
+            c.tile = pl.tile_bytes;
+            c.wpb = best_w;
+            c.per_sm = best_ps;
         }
-        if (c.per_sm < 1) return RASP_ECAPACITY;
+        pl.warps_per_block = c.wpb;
+        pl.dyn_smem = pl.tile_bytes * size_t(c.wpb);
         pl.blocks = c.per_sm * dv.nsm;
     }
+    const int threads = 32 * pl.warps_per_block;
     const uint64_t tiles = (d + 31) / 32;
     const uint64_t need_blocks = (tiles + pl.warps_per_block - 1) / pl.warps_per_block;
     const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(pl.blocks), need_blocks)));

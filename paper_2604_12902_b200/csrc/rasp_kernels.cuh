@@ -158,14 +158,32 @@ __device__ __forceinline__ uint4 get16(const SC *col, uint32_t k)
     return make_uint4(wv[0], wv[1], wv[2], wv[3]);
 }
 
+// Loads are issued in batches (8 x 16 B, or 8 scalars) before any of the
+// dependent shared-memory stores, so a row costs ~one DRAM latency instead
+// of one per chunk.
 template <class S, class SC>
 __device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t ncells, SC *col)
 {
     constexpr uint32_t PER = 16 / sizeof(S);
+    constexpr uint32_t B = 8;
     uint32_t k = 0;
     if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
         const uint4 *v = reinterpret_cast<const uint4 *>(row);
+        for (; k + B * PER <= ncells; k += B * PER) {
+            uint4 q[B];
+#pragma unroll
+            for (uint32_t j = 0; j < B; ++j) q[j] = v[k / PER + j];
+#pragma unroll
+            for (uint32_t j = 0; j < B; ++j) put16<S, SC>(col, k + j * PER, q[j]);
+        }
         for (; k + PER <= ncells; k += PER) put16<S, SC>(col, k, v[k / PER]);
+    }
+    for (; k + B <= ncells; k += B) {
+        S e[B];
+#pragma unroll
+        for (uint32_t j = 0; j < B; ++j) e[j] = row[k + j];
+#pragma unroll
+        for (uint32_t j = 0; j < B; ++j) col[(k + j) * 32] = static_cast<SC>(e[j]);
     }
     for (; k < ncells; ++k) col[k * 32] = static_cast<SC>(row[k]);
 }
