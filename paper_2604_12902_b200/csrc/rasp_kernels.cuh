@@ -239,8 +239,8 @@ __device__ __forceinline__ CT ld_cell(char *base, uint32_t a)
 {
     if constexpr (SMEM) {
         if constexpr (sizeof(SC) == 2) {
-            unsigned short v;
-            asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(a));
+            uint32_t v;   // zero-extending 16-bit load straight into a 32-bit register
+            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
             return static_cast<CT>(v);
         } else if constexpr (sizeof(SC) == 4) {
             uint32_t v;
@@ -403,7 +403,9 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
              (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * static_cast<size_t>(tile_bytes);
         lm = lane * static_cast<uint32_t>(sizeof(SC));
     }
-    const Opq q = {A.one, A.two, A.row};
+    // per-thread copies (threadIdx.x >> 10 == 0): not uniform, so adds stay on IMAD
+    const uint32_t tz = threadIdx.x >> 10;
+    const Opq q = {A.one + tz, A.two + tz, A.row + tz};
     const uint32_t U = n * ROW + lm;                       // u[1] of this lane
     const uint32_t Y = (n + A.g.ell + 1) * ROW + lm;       // y[1] of this lane (epoch scratch)
     // generic base for the (cold) row copies: gb + address = generic pointer
