@@ -36,9 +36,18 @@ typedef struct {
     u64 wmask, n, ell, s;
 } oracle_state;
 
+/* x mod n with a 32-bit divide when both fit (the same value; 64-bit
+ * division is several times slower on x86, which LLVM -- and so the numba
+ * reference -- also special-cases). */
+static inline u64 umod(u64 x, u64 n)
+{
+    if (((x | n) >> 32) == 0) return (uint32_t)x % (uint32_t)n;
+    return x % n;
+}
+
 /* hypervisor.py:72-125.  Returns 1 iff VM j is at a fixed point; otherwise
  * applies one step when do_apply. */
-static int oracle_advance(const oracle_state *st, i64 j, int do_apply)
+static inline int oracle_advance(const oracle_state *st, i64 j, int do_apply)
 {
     const u64 n = st->n, wmask = st->wmask;
     u64 *Mj = st->M + (size_t)j * n;
@@ -46,9 +55,9 @@ static int oracle_advance(const oracle_state *st, i64 j, int do_apply)
     u64 *yj = st->y + (size_t)j * (st->s + 1);
     const u64 i0 = st->iw[j];
     const u64 a0 = st->ac[j];
-    const u64 o = Mj[i0 % n];                       /* hv:78 */
-    const u64 jw = Mj[((i0 + 1) & wmask) % n];      /* hv:79 */
-    const u64 jn = jw % n;                          /* hv:80 */
+    const u64 o = Mj[umod(i0, n)];                       /* hv:78 */
+    const u64 jw = Mj[umod((i0 + 1) & wmask, n)];        /* hv:79 */
+    const u64 jn = umod(jw, n);                          /* hv:80 */
     const u64 mj = Mj[jn];                          /* hv:81 */
     const u64 u0 = uj[0], y0 = yj[0];
 
@@ -83,6 +92,59 @@ static int oracle_advance(const oracle_state *st, i64 j, int do_apply)
     return 0;
 }
 
+/* One visit of machine j (the body of the `while applied < q` loop of
+ * hypervisor.py:138-154): up to q steps with i, a and the cursors held in
+ * locals, exactly the per-step logic of oracle_advance (hv:72-125).
+ * Returns the new status (RUNNING if the visit ended on q). */
+static int oracle_visit(const oracle_state *st, i64 j, i64 q, i64 tau_max)
+{
+    const u64 n = st->n, wmask = st->wmask, ell = st->ell, s = st->s;
+    u64 *Mj = st->M + (size_t)j * n;
+    u64 *uj = st->u + (size_t)j * (ell + 1);
+    u64 *yj = st->y + (size_t)j * (s + 1);
+    u64 i0 = st->iw[j], a0 = st->ac[j], u0 = uj[0], y0 = yj[0];
+    i64 steps = st->steps[j];
+    int status = RUNNING;
+    for (i64 applied = 0; applied < q; ++applied) {
+        const u64 o = Mj[umod(i0, n)];
+        const u64 jw = Mj[umod((i0 + 1) & wmask, n)];
+        const u64 jn = umod(jw, n);
+        const u64 mj = Mj[jn];
+        u64 ni = (i0 + 2) & wmask, na = a0, nm = mj, nu0 = u0, ny0 = y0;
+        int write_out = 0;
+        switch (o) {
+        case 1: na = jw; break;
+        case 2: na = (a0 + mj) & wmask; break;
+        case 3: na = (a0 * mj) & wmask; break;
+        case 4: nm = a0; break;
+        case 5: if (a0 != 0) ni = jw; break;
+        case 6:
+            if (u0 < ell) { nm = uj[u0 + 1]; nu0 = u0 + 1; }
+            else ni = i0;
+            break;
+        case 7:
+            if (y0 < s) { ny0 = y0 + 1; write_out = 1; }
+            break;
+        default: ni = i0;
+        }
+        const int fixed = ni == i0 && na == a0 && nm == mj && nu0 == u0 && ny0 == y0;
+        if (steps >= tau_max) {                      /* hv:140-148: probe only */
+            status = fixed ? HALTED : EXHAUSTED;
+            break;
+        }
+        if (fixed) { status = HALTED; break; }       /* hv:149-152 */
+        i0 = ni; a0 = na; Mj[jn] = nm; u0 = nu0;     /* hv:117-124 */
+        if (write_out) yj[y0 + 1] = mj;
+        y0 = ny0;
+        ++steps;                                     /* hv:153 */
+    }
+    st->iw[j] = i0; st->ac[j] = a0; uj[0] = u0; yj[0] = y0;
+    st->steps[j] = steps;
+    if (status == HALTED) st->tau_h[j] = steps;
+    if (status != RUNNING) st->status[j] = (int8_t)status;
+    return status;
+}
+
 /* hypervisor.py:128-164: stripe {g + kW}, `rounds` sweeps of at most q
  * steps per visit, budget probe, final classification sweep. */
 void oracle_worker(const oracle_state *st, i64 g, i64 W, i64 q, i64 rounds, i64 tau_max)
@@ -93,25 +155,7 @@ void oracle_worker(const oracle_state *st, i64 g, i64 W, i64 q, i64 rounds, i64 
         for (i64 k = 0; k < stripe; ++k) {
             const i64 j = g + k * W;
             if (st->status[j] != RUNNING) continue;
-            i64 applied = 0;
-            while (applied < q) {
-                if (st->steps[j] >= tau_max) {           /* hv:140-148 */
-                    if (oracle_advance(st, j, 0)) {
-                        st->status[j] = HALTED;
-                        st->tau_h[j] = st->steps[j];
-                    } else {
-                        st->status[j] = EXHAUSTED;
-                    }
-                    break;
-                }
-                if (oracle_advance(st, j, 1)) {          /* hv:149-152 */
-                    st->status[j] = HALTED;
-                    st->tau_h[j] = st->steps[j];
-                    break;
-                }
-                st->steps[j] += 1;                      /* hv:153-154 */
-                applied += 1;
-            }
+            oracle_visit(st, j, q, tau_max);
         }
     }
     for (i64 k = 0; k < stripe; ++k) {                   /* hv:157-164 */
