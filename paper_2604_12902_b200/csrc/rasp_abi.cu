@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include <atomic>
@@ -225,6 +226,10 @@ int dispatch_flags(const rasp_params *p, const rasp::EpochArgs &a, const Plan &p
             if (pow2) return dispatch_budget<S, SC, CT, true, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
             return dispatch_budget<S, SC, CT, false, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
         }
+        if (p->w == 16) {
+            if (pow2) return dispatch_budget<S, SC, CT, true, Arith::CELL>(a, pl, dv, ws, d, tau_max, epoch, st);
+            return dispatch_budget<S, SC, CT, false, Arith::CELL>(a, pl, dv, ws, d, tau_max, epoch, st);
+        }
     } else {
         if (p->w == 8 * sizeof(CT)) {
             if (pow2) return dispatch_budget<S, SC, CT, true, Arith::FULL>(a, pl, dv, ws, d, tau_max, epoch, st);
@@ -334,6 +339,8 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.one = 1;
     a.two = 2;
     a.row = uint32_t(32 * cell_bytes(p->w));
+    a.stable_q8 = 128;                       // 0.5 (measured best on C2 and C5): tuning knob RASP_STABLE_Q8
+    if (const char *e = std::getenv("RASP_STABLE_Q8")) a.stable_q8 = uint32_t(std::strtoul(e, nullptr, 10));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!a.inplace) {
         // out-of-place: the input tapes and the bookkeeping arrays move in bulk;

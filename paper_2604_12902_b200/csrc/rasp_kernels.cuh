@@ -34,8 +34,11 @@ constexpr unsigned kFull = 0xffffffffu;
 constexpr int8_t kRunning = 0, kHalted = 1, kExhausted = 2;
 
 // Word arithmetic regime: w == 1 (generic fixedness test), 2 <= w < bits(CT)
-// (masked), w == bits(CT) (native wrap-around, no masks).
-enum class Arith { W1, NARROW, FULL };
+// (masked), w == bits(CT) (native wrap-around, no masks), and CELL: w equals
+// the tile cell width but not bits(CT) (w = 16 on u16 cells) -- the
+// accumulator then carries garbage above bit w between steps (every store
+// truncates to the cell, every test masks), which saves the masks on ADD/MUL.
+enum class Arith { W1, NARROW, FULL, CELL };
 
 struct Geo {
     uint64_t mask;    // 2^w - 1
@@ -86,6 +89,7 @@ struct EpochArgs {
     uint32_t tile_rows;            // n + ell + 1 + s
     uint32_t one, two;             // the constants 1 and 2 (see Opq)
     uint32_t row;                  // bytes per tile row (32 * sizeof(SC))
+    uint32_t stable_q8;            // survival ratio (x256) at which the rest runs as one epoch
 };
 
 template <class CT, Arith AR>
@@ -318,7 +322,7 @@ __device__ __forceinline__ bool is_fixed(const LaneState<CT> &L, const Fetch<CT>
                                          uint32_t yend, const Geo &g, const Opq &q)
 {
     const CT mask = static_cast<CT>(g.mask);
-    const bool taken = (f.o == 5) & (L.a != 0);
+    const bool taken = (f.o == 5) & ((AR == Arith::CELL ? (L.a & mask) : L.a) != 0);
     const bool ucap = L.ua >= uend;
     if constexpr (AR != Arith::W1) {
         bool self;
@@ -360,8 +364,13 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
     const bool app = L.active & can_apply;
     // commit: every update is a predicated move/store keyed on its own case
     if (app & (f.o == 1)) L.a = f.jw;
-    if (app & (f.o == 2)) L.a = wrap<CT, AR>(a0 + f.mj, mask);
-    if (app & (f.o == 3)) L.a = wrap<CT, AR>(a0 * f.mj, mask);
+    if constexpr (AR == Arith::CELL) {   // low w bits exact; masked at every test
+        if (app & (f.o == 2)) L.a = a0 + f.mj;
+        if (app & (f.o == 3)) L.a = a0 * f.mj;
+    } else {
+        if (app & (f.o == 2)) L.a = wrap<CT, AR>(a0 + f.mj, mask);
+        if (app & (f.o == 3)) L.a = wrap<CT, AR>(a0 * f.mj, mask);
+    }
     if (app & (f.o == 4)) st_cell<SC, CT, SMEM>(base, f.jo, a0);
     const bool rd = (f.o == 6) & (L.ua < uend);
     if (app & rd) {
@@ -373,7 +382,7 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
         L.ya += q.row;
     }
     if (app) {
-        const bool taken = (f.o == 5) & (a0 != 0);
+        const bool taken = (f.o == 5) & ((AR == Arith::CELL ? (a0 & mask) : a0) != 0);
         CT i2;
         if constexpr (kRawI<POW2, AR>) i2 = L.i + static_cast<CT>(q.two);
         else i2 = wrap<CT, AR>(L.i + 2, mask);
@@ -507,6 +516,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const uint32_t u0 = (L.ua - U) / ROW;
             const uint32_t y0 = (L.ya - Y) / ROW;
             if constexpr (kRawI<POW2, AR>) L.i &= static_cast<CT>(A.g.mask);
+            if constexpr (AR == Arith::CELL) L.a &= static_cast<CT>(A.g.mask);
             S *dY = static_cast<S *>(dst.y) + id * ycols;
             const SC *colY = reinterpret_cast<const SC *>(gb + Y);
             for (uint32_t k = y0_start; k < y0; ++k) dY[k + 1] = static_cast<S>(colY[k * 32]);
@@ -559,9 +569,9 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const int64_t left = A.tau_max - cov;
             uint32_t kn = 0;
             if (cout > 0 && left > 0 && ntiles > 0) {
-                // survivors that mostly keep running get the whole remaining
-                // budget in one epoch; otherwise keep compacting at 2x length
-                const bool stable = 4ull * cout >= 3ull * count;
+                // once at least stable_q8/256 of the live set survives an epoch
+                // the rest runs as one epoch; otherwise keep compacting at 2x length
+                const bool stable = 256ull * cout >= static_cast<uint64_t>(A.stable_q8) * count;
                 const uint64_t want = stable ? static_cast<uint64_t>(left)
                                              : 2ull * (K > 0 ? K : 1u);
                 kn = static_cast<uint32_t>(min(min(want, static_cast<uint64_t>(left)),
