@@ -95,6 +95,22 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out,
              int64_t tau_max, int64_t epoch, uint32_t flags,
              void *workspace, size_t workspace_bytes, void *stream);
 
+/* Device packer of init_config (machine.py:289-309) for a whole batch:
+ * M = program || 0, u = (0, inputs || 0), y = 0, i = a = 0, status = 0,
+ * steps = 0, tau_h = -1.  programs: [d][prog_len], inputs: [d][input_len],
+ * both device buffers of out->word_bytes words (range-checked by the caller).
+ * Lets a caller ship only programs and inputs over PCIe. */
+int rasp_init_c0(const rasp_params *p, const void *programs, uint32_t prog_len,
+                 const void *inputs, uint32_t input_len, const rasp_batch *out, void *stream);
+
+/* Generator G_dev (SURVEY §8d generator G, on the device): every program
+ * fills memory with opcode/operand pairs (opcode uniform in 1..7, operand
+ * uniform in [0, n), BNZ operands even), ell uniform input words, i = a = 0.
+ * Machine j of the batch is machine first_machine + j of the stream `seed`
+ * (counter-based splitmix64), so shards generate independently. */
+int rasp_generate(const rasp_params *p, uint64_t seed, uint64_t first_machine,
+                  const rasp_batch *out, void *stream);
+
 /* Exhaustive program enumeration (BASELINE config 4).
  * Program rank r: pair k = bits [k*(ob+pb), (k+1)*(ob+pb)) of r, opcode = the
  * low ob bits, operand = the next pb bits.  Machine (r, x) is

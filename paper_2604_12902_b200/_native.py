@@ -22,7 +22,7 @@ RASP_FRESH = 1
 # symbols declared by include/raspvisor_b200.h
 EXPORTS = ("rasp_workspace_bytes", "rasp_run", "rasp_histogram", "rasp_validate",
            "rasp_error_string", "rasp_last_cuda_error", "rasp_abi_version",
-           "rasp_launch_count", "rasp_enumerate")
+           "rasp_launch_count", "rasp_enumerate", "rasp_init_c0", "rasp_generate")
 
 
 class RaspParams(ctypes.Structure):
@@ -80,6 +80,10 @@ def load():
     lib.rasp_abi_version.restype = ctypes.c_int
     lib.rasp_enumerate.argtypes = [ctypes.POINTER(RaspEnumParams), U64, U64, P, P, P]
     lib.rasp_enumerate.restype = ctypes.c_int
+    lib.rasp_init_c0.argtypes = [pp, P, U32, P, U32, pb, P]
+    lib.rasp_init_c0.restype = ctypes.c_int
+    lib.rasp_generate.argtypes = [pp, U64, U64, pb, P]
+    lib.rasp_generate.restype = ctypes.c_int
     lib.rasp_launch_count.argtypes = []
     lib.rasp_launch_count.restype = ctypes.c_ulonglong
     if lib.rasp_abi_version() != ABI_VERSION:

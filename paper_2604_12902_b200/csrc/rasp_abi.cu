@@ -418,6 +418,62 @@ int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t cou
     return RASP_OK;
 }
 
+int rasp_init_c0(const rasp_params *p, const void *programs, uint32_t prog_len, const void *inputs,
+                 uint32_t input_len, const rasp_batch *out, void *stream)
+{
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!out || (prog_len && !programs) || (input_len && !inputs)) return RASP_EPARAM;
+    if (prog_len > p->n || input_len > p->ell) return RASP_ECAPACITY;
+    const uint32_t wb = out->word_bytes;
+    if ((wb != 1 && wb != 2 && wb != 4 && wb != 8) || wb < natural_bytes(p->w)) return RASP_EDTYPE;
+    if (out->d == 0) return RASP_OK;
+    Device dv;
+    rc = device_info(dv);
+    if (rc) return rc;
+    const unsigned blocks = unsigned(std::min<uint64_t>((out->d * p->n + 255) / 256, uint64_t(dv.nsm) * 16));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const rasp::Side sd = side_of(out);
+    const uint32_t ell = uint32_t(p->ell), s = uint32_t(p->s);
+    switch (wb) {
+    case 1: rasp::init_c0_kernel<uint8_t><<<blocks, 256, 0, st>>>(sd, out->d, p->n, ell, s, static_cast<const uint8_t *>(programs), prog_len, static_cast<const uint8_t *>(inputs), input_len); break;
+    case 2: rasp::init_c0_kernel<uint16_t><<<blocks, 256, 0, st>>>(sd, out->d, p->n, ell, s, static_cast<const uint16_t *>(programs), prog_len, static_cast<const uint16_t *>(inputs), input_len); break;
+    case 4: rasp::init_c0_kernel<uint32_t><<<blocks, 256, 0, st>>>(sd, out->d, p->n, ell, s, static_cast<const uint32_t *>(programs), prog_len, static_cast<const uint32_t *>(inputs), input_len); break;
+    default: rasp::init_c0_kernel<uint64_t><<<blocks, 256, 0, st>>>(sd, out->d, p->n, ell, s, static_cast<const uint64_t *>(programs), prog_len, static_cast<const uint64_t *>(inputs), input_len); break;
+    }
+    RASP_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return RASP_OK;
+}
+
+int rasp_generate(const rasp_params *p, uint64_t seed, uint64_t first_machine, const rasp_batch *out,
+                  void *stream)
+{
+    int rc = check_params(p);
+    if (rc) return rc;
+    if (!out) return RASP_EPARAM;
+    const uint32_t wb = out->word_bytes;
+    if ((wb != 1 && wb != 2 && wb != 4 && wb != 8) || wb < natural_bytes(p->w)) return RASP_EDTYPE;
+    if (out->d == 0) return RASP_OK;
+    Device dv;
+    rc = device_info(dv);
+    if (rc) return rc;
+    const unsigned blocks = unsigned(std::min<uint64_t>((out->d * p->n + 255) / 256, uint64_t(dv.nsm) * 16));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const rasp::Side sd = side_of(out);
+    const uint64_t mask = p->w == 64 ? ~0ull : ((1ull << p->w) - 1);
+    const uint32_t ell = uint32_t(p->ell), s = uint32_t(p->s);
+    switch (wb) {
+    case 1: rasp::generate_kernel<uint8_t><<<blocks, 256, 0, st>>>(sd, out->d, first_machine, p->n, ell, s, mask, seed); break;
+    case 2: rasp::generate_kernel<uint16_t><<<blocks, 256, 0, st>>>(sd, out->d, first_machine, p->n, ell, s, mask, seed); break;
+    case 4: rasp::generate_kernel<uint32_t><<<blocks, 256, 0, st>>>(sd, out->d, first_machine, p->n, ell, s, mask, seed); break;
+    default: rasp::generate_kernel<uint64_t><<<blocks, 256, 0, st>>>(sd, out->d, first_machine, p->n, ell, s, mask, seed); break;
+    }
+    RASP_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return RASP_OK;
+}
+
 int rasp_histogram(const int8_t *status, const int64_t *tau_h, uint64_t d, int64_t *out, void *stream)
 {
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -721,6 +721,83 @@ enum_kernel(const EnumArgs A)
     }
 }
 
+// --- on-device c0 construction -----------------------------------
+//
+// init_c0_kernel: the device packer of init_config (m:289-309) for a batch:
+//   M = P_j || 0^(n-L), u = (0, x_j || 0^(ell-k)), y = 0^(s+1), i = a = 0,
+//   status = 0, steps = 0, tau_h = -1.  Programs [d][L] and inputs [d][k] in
+//   the batch word type; ranges are checked by the host surface beforehand.
+// generate_kernel: generator G_dev, the device twin of generator G (SURVEY
+//   §8d): program fills memory, even cells opcode uniform in 1..7, odd cells
+//   operand uniform in [0, n) (BNZ operands even), ell random input words.
+//   Counter-based (splitmix64 of (seed, machine, cell)), so any shard of any
+//   size is generated independently; not bit-identical to numpy's G.
+
+template <class S>
+__global__ void init_c0_kernel(Side b, uint64_t d, uint32_t n, uint32_t ell, uint32_t s,
+                               const S *__restrict__ prog, uint32_t L, const S *__restrict__ inp,
+                               uint32_t k)
+{
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    S *M = static_cast<S *>(b.M), *u = static_cast<S *>(b.u), *y = static_cast<S *>(b.y);
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < d * n; t += stride) {
+        const uint64_t j = t / n, c = t % n;
+        M[t] = c < L ? prog[j * L + c] : S(0);
+    }
+    const uint64_t uc = static_cast<uint64_t>(ell) + 1, yc = static_cast<uint64_t>(s) + 1;
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < d * uc; t += stride) {
+        const uint64_t j = t / uc, c = t % uc;
+        u[t] = (c >= 1 && c <= k) ? inp[j * k + (c - 1)] : S(0);
+    }
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < d * yc; t += stride)
+        y[t] = S(0);
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < d; j += stride) {
+        static_cast<S *>(b.iw)[j] = S(0);
+        static_cast<S *>(b.ac)[j] = S(0);
+        b.status[j] = kRunning;
+        b.steps[j] = 0;
+        b.tau_h[j] = -1;
+    }
+}
+
+__device__ __forceinline__ uint64_t mix64(uint64_t z);
+
+template <class S>
+__global__ void generate_kernel(Side b, uint64_t d, uint64_t first, uint32_t n, uint32_t ell,
+                                uint32_t s, uint64_t mask, uint64_t seed)
+{
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    S *M = static_cast<S *>(b.M), *u = static_cast<S *>(b.u), *y = static_cast<S *>(b.y);
+    const uint64_t key = mix64(seed ^ 0x5241535056495352ull);   // "RASPVISR"
+    const uint32_t half = n / 2;
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < d * half; t += stride) {
+        const uint64_t j = t / half, c = t % half;
+        const uint64_t r = mix64(key ^ mix64(((first + j) << 20) ^ (c << 1)));
+        const uint64_t op = 1 + (r & 0xffffffffull) % 7;
+        uint64_t opr = (r >> 32) % n;
+        if (op == 5) opr &= ~1ull;
+        M[j * n + 2 * c] = static_cast<S>(op & mask);
+        M[j * n + 2 * c + 1] = static_cast<S>(opr & mask);
+    }
+    if (n & 1)
+        for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < d; j += stride)
+            M[j * n + n - 1] = S(0);
+    const uint64_t uc = static_cast<uint64_t>(ell) + 1, yc = static_cast<uint64_t>(s) + 1;
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < d * uc; t += stride) {
+        const uint64_t j = t / uc, c = t % uc;
+        u[t] = c == 0 ? S(0) : static_cast<S>(mix64(key ^ mix64(((first + j) << 20) ^ (c << 1) ^ 1)) & mask);
+    }
+    for (uint64_t t = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; t < d * yc; t += stride)
+        y[t] = S(0);
+    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < d; j += stride) {
+        static_cast<S *>(b.iw)[j] = S(0);
+        static_cast<S *>(b.ac)[j] = S(0);
+        b.status[j] = kRunning;
+        b.steps[j] = 0;
+        b.tau_h[j] = -1;
+    }
+}
+
 // Bulk device copy on the SMs (keeps the copy engines free for host traffic).
 __global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ dst, uint64_t n16,
                             const unsigned char *__restrict__ srcb, unsigned char *__restrict__ dstb,

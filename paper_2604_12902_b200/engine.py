@@ -158,6 +158,35 @@ class Engine:
         _native.check(rc, "rasp_run")
         return dst
 
+    def init_c0(self, programs: torch.Tensor, inputs: torch.Tensor, out: DeviceBatch, stream=None) -> DeviceBatch:
+        """Device packer of init_config (rasp_init_c0): programs [d, L] and
+        inputs [d, k] device tensors of the batch word type -> c0 in `out`.
+        Words must already be range-checked (see machine.init_batch)."""
+        if programs.shape[0] != out.d or (inputs.numel() and inputs.shape[0] != out.d):
+            raise ValueError("programs/inputs must have one row per machine")
+        L = programs.shape[1] if programs.dim() == 2 else 0
+        k = inputs.shape[1] if inputs.dim() == 2 else 0
+        if L > self.params.n:
+            raise CapacityError(f"program needs {L} memory words but n = {self.params.n}")
+        if k > self.params.ell:
+            raise CapacityError(f"input vector has {k} words but ell = {self.params.ell}")
+        b = out.c_struct()
+        with torch.cuda.device(self.device):
+            rc = self.lib.rasp_init_c0(ctypes.byref(self._p), programs.data_ptr() if L else None, L,
+                                       inputs.data_ptr() if k else None, k, ctypes.byref(b),
+                                       self._stream_ptr(stream))
+        _native.check(rc, "rasp_init_c0")
+        return out
+
+    def generate(self, out: DeviceBatch, seed: int, first_machine: int = 0, stream=None) -> DeviceBatch:
+        """Generator G_dev on the device (rasp_generate): fresh c0 in `out`."""
+        b = out.c_struct()
+        with torch.cuda.device(self.device):
+            rc = self.lib.rasp_generate(ctypes.byref(self._p), int(seed), int(first_machine),
+                                        ctypes.byref(b), self._stream_ptr(stream))
+        _native.check(rc, "rasp_generate")
+        return out
+
     def histogram(self, batch: DeviceBatch, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
         """int64[102] device tensor: tau_h 0..99, 100+, nonhalt (rasp_histogram)."""
         h = out if out is not None else torch.empty(102, dtype=torch.int64, device=self.device)

@@ -41,3 +41,30 @@ def synthetic_c0(d: int, params: MachineParams, seed: int = 0, dtype=None) -> di
         "u": u,
         "y": np.zeros((d, s + 1), dt),
     }
+
+
+def random_configs(count: int, params: MachineParams, rng: np.random.Generator, dtype=None) -> dict:
+    """Well-formed mid-run configurations (not c0): arbitrary i, a, cursors and
+    tapes, opcode cells biased into [0, 9) -- the distribution of the
+    reference's differential corpus (selftest.py:32-95), drawn as SoA arrays.
+    Used to exercise every step case at scale."""
+    w, n, ell, s = params.w, params.n, params.ell, params.s
+    top = (1 << w) - 1
+    dt = np.dtype(dtype) if dtype is not None else natural_dtype(w)
+
+    def words(shape):
+        return rng.integers(0, top, shape, dtype=np.uint64, endpoint=True)
+
+    M = words((count, n))
+    half = (n + 1) // 2
+    ops = rng.integers(0, 9, (count, half), dtype=np.uint64) % np.uint64(top + 1 if w < 64 else 1 << 63)
+    keep = rng.random((count, half)) < 0.8
+    M[:, 0::2] = np.where(keep, ops, M[:, 0::2])
+    u = np.concatenate([rng.integers(0, ell + 1, (count, 1), dtype=np.uint64), words((count, ell))], 1)
+    y = np.concatenate([rng.integers(0, s + 1, (count, 1), dtype=np.uint64), words((count, s))], 1)
+    near = rng.integers(0, 2 * n, count, dtype=np.uint64) & np.uint64(top)
+    i = np.where(rng.random(count) < 0.7, near, words(count))
+    small = rng.integers(0, min(top + 1, 10), count, dtype=np.uint64)
+    a = np.where(rng.random(count) < 0.5, small, words(count))
+    return {"iw": i.astype(dt), "ac": a.astype(dt), "M": M.astype(dt), "u": u.astype(dt),
+            "y": y.astype(dt)}

@@ -183,3 +183,94 @@ def test_large_batch_against_oracle_sample(pkg):
     res2 = H.run_arrays(c0, p, H.BatchConfig(tau_max=tau, epoch=5, memory_budget_words=1 << 40))
     for k in RESULTS:
         assert np.array_equal(getattr(res2.slots, k), getattr(sv, k)), k
+
+
+@pytest.mark.parametrize("shape", [(8, 8, 2, 2), (16, 16, 2, 2), (16, 64, 8, 8), (32, 250, 10, 2),
+                                   (32, 64, 4, 2), (64, 12, 3, 3), (5, 7, 3, 2), (1, 6, 1, 1)])
+def test_random_midrun_configs_against_oracle(pkg, shape):
+    """Arbitrary mid-run configurations (every step case, odd i, full tapes,
+    wrapped addresses) at 8K machines per shape, several epochs."""
+    P, H = pkg
+    from oracle import oracle
+    from paper_2604_12902_b200.workload import random_configs
+    w, n, ell, s = shape
+    p = P.MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
+    c0 = random_configs(8192, p, np.random.default_rng(w * 1000 + n))
+    for tau in (0, 3, 200):
+        want = oracle.worker_arrays(c0, w, n, ell, s, tau)
+        for epoch in (1, 64):
+            res = H.run_arrays(c0, p, H.BatchConfig(tau_max=tau, epoch=epoch))
+            for k in RESULTS:
+                got = np.asarray(getattr(res.slots, k))
+                if k in FIELDS:
+                    got = got.astype(np.uint64)
+                np.testing.assert_array_equal(got, want[k], err_msg=f"{shape} tau={tau} {k}")
+
+
+def test_device_packer_matches_init_batch(pkg):
+    import torch
+    P, H = pkg
+    from paper_2604_12902_b200.engine import DeviceBatch
+    p = P.MachineParams(w=16, n=64, ell=8, s=8, mu=1)
+    rng = np.random.default_rng(3)
+    progs = rng.integers(0, 1 << 16, (1000, 40), dtype=np.uint64).astype(np.uint16)
+    xs = rng.integers(0, 1 << 16, (1000, 5), dtype=np.uint64).astype(np.uint16)
+    want = P.init_batch(progs, xs, p)
+    out = DeviceBatch.empty(1000, p, fresh=False)
+    eng = H.get_engine(p)
+    eng.init_c0(torch.from_numpy(progs).cuda(), torch.from_numpy(xs).cuda(), out)
+    got = out.to_numpy()
+    for k in FIELDS:
+        np.testing.assert_array_equal(got[k], want[k], err_msg=k)
+    assert not got["status"].any() and not got["steps"].any() and (got["tau_h"] == -1).all()
+
+
+def test_device_generator_shape_and_parity(pkg):
+    """G_dev: the c0 shape of generator G, deterministic per (seed, machine),
+    shard-independent; runs bit-exactly against the oracle."""
+    P, H = pkg
+    from oracle import oracle
+    from paper_2604_12902_b200.engine import DeviceBatch
+    p = P.MachineParams(w=16, n=64, ell=8, s=8, mu=1)
+    eng = H.get_engine(p)
+    a = eng.generate(DeviceBatch.empty(4096, p, fresh=False), seed=7).to_numpy()
+    b = eng.generate(DeviceBatch.empty(1024, p, fresh=False), seed=7, first_machine=3072).to_numpy()
+    for k in FIELDS:
+        np.testing.assert_array_equal(a[k][3072:], b[k])
+    ops, opr = a["M"][:, 0::2], a["M"][:, 1::2]
+    assert ops.min() >= 1 and ops.max() <= 7 and opr.max() < 64
+    assert (opr[ops == 5] % 2 == 0).all()
+    assert set(np.unique(ops)) == set(range(1, 8))
+    assert not a["iw"].any() and not a["u"][:, 0].any() and not a["y"].any()
+    c0 = {k: a[k] for k in FIELDS}
+    res = H.run_arrays(c0, p, H.BatchConfig(tau_max=1024))
+    want = oracle.worker_arrays(c0, p.w, p.n, p.ell, p.s, 1024)
+    for k in RESULTS:
+        got = np.asarray(getattr(res.slots, k))
+        if k in FIELDS:
+            got = got.astype(np.uint64)
+        np.testing.assert_array_equal(got, want[k], err_msg=k)
+
+
+def test_scalar_path_through_kernel(pkg):
+    """step / run_to_fixpoint (m:169-211, m:336-357 signatures) on the GPU:
+    the step KATs of t/test_machine.py:90-166 and the trace example :202-208."""
+    P, H = pkg
+    from golden_io import load_raw
+    from paper_2604_12902_b200 import scalar
+    z = load_raw("kat")
+    g = load_family("kat")[0]
+    p = _params(P, g)
+    for k in range(g.d):
+        c = P.Config(int(g.c0["iw"][k]), int(g.c0["ac"][k]), tuple(int(v) for v in g.c0["M"][k]),
+                     tuple(int(v) for v in g.c0["u"][k]), tuple(int(v) for v in g.c0["y"][k]))
+        out = scalar.step(c, p)
+        flat = [out.next.i, out.next.a, *out.next.M, *out.next.u, *out.next.y]
+        assert flat == [int(v) for v in z["step_next"][k]], k
+        assert out.fixed_point == bool(z["step_fixed"][k]), k
+    c0 = P.init_config(P.Program((1, 5, 4, 6)), [], p)
+    seen = []
+    cf, tau = scalar.run_to_fixpoint(c0, 10, p, trace=lambda t, c: seen.append((t, c.i)))
+    assert seen == [(0, 0), (1, 2), (2, 4)] and tau == 2 and cf.M[6] == 5
+    assert scalar.run_to_fixpoint(c0, 1, p)[1] is None
+    assert scalar.run_to_fixpoint(c0, 2, p)[1] == 2
