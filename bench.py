@@ -47,6 +47,12 @@ CONFIGS = {
            "16M random programs/GPU, w=16 n=64 l=8 s=8, run to halt (cap 1024)"),
     "c5": (1 << 20, 32, 256, 32, 32, 1024,
            "1M random programs/GPU, w=32 n=256 l=32 s=32, divergent halting (cap 1024)"),
+    # the paper protocol's geometry with the 64
+    # programs the reference's sampler+compiler produce for L=30 (golden fixture),
+    # tiled to 1M machines with fresh random inputs, tau 10^4
+    "paper": (1 << 20, 32, 250, 10, 2, 10000,
+              "1M machines: 64 sampled+lowered L=30 programs (reference build_workload) x random "
+              "inputs, w=32 n=250 l=10 s=2, tau 10^4"),
     # d = programs; machines = programs x 2^w inputs (SURVEY §8d C4 domain)
     "c4": (1 << 28, 8, 16, 1, 1, 64,
            "exhaustive: all 2^28 programs of m=4 pairs (3-bit opcode, 4-bit operand), w=8 n=16, "
@@ -123,6 +129,25 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def make_c0(cfg_name, d, p, seed):
+    """Host c0 for a config: generator G, or the paper-protocol programs."""
+    from paper_2604_12902_b200.workload import synthetic_c0
+    if cfg_name != "paper":
+        return synthetic_c0(d, p, seed=seed)
+    z = np.load(os.path.join(ROOT, "tests", "golden", "paper.npz"))
+    M0, u0 = z["g000_c0_M"].astype(np.uint32), z["g000_c0_u"].astype(np.uint32)
+    reps = -(-d // M0.shape[0])
+    M = np.tile(M0, (reps, 1))[:d]
+    u = np.tile(u0, (reps, 1))[:d]
+    rng = np.random.default_rng(seed)
+    fresh = rng.integers(0, 1 << 32, u.shape, dtype=np.uint64).astype(np.uint32)
+    used = np.tile((u0 != 0), (reps, 1))[:d]
+    used[:, 0] = False
+    u = np.where(used, fresh, u)
+    return {"iw": np.zeros(d, np.uint32), "ac": np.zeros(d, np.uint32), "M": np.ascontiguousarray(M),
+            "u": np.ascontiguousarray(u), "y": np.zeros((d, p.s + 1), np.uint32)}
+
+
 def cpu_reference(cfg_name, steps_k, warmup, sample_d=None, seed=0):
     """Time the reference algorithm on the host (oracle port, all threads)."""
     from oracle import oracle
@@ -149,7 +174,7 @@ def cpu_reference(cfg_name, steps_k, warmup, sample_d=None, seed=0):
                 "seconds": best}
     sample = min(d, sample_d or (1 << 16))
     p = MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
-    c0 = synthetic_c0(sample, p, seed=seed)
+    c0 = make_c0(cfg_name, sample, p, seed)
     for it in range(warmup + steps_k):
         t0 = time.perf_counter()
         out = oracle.worker_arrays(c0, w, n, ell, s, tau, epoch=64, workers=cores)
@@ -285,7 +310,9 @@ def main():
             "ms_per_step": cb["seconds"] * 1e3, "higher_is_better": True,
             "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "u64",
-            "data": "exhaustive enumeration" if args.config == "c4" else "synthetic (generator G)",
+            "data": {"c4": "exhaustive enumeration",
+                     "paper": "reference-sampled programs x random inputs"}.get(args.config,
+                                                                              "synthetic (generator G)"),
             "config": {"workload": args.config, "desc": desc, "w": w, "n": n, "ell": ell, "s": s,
                        "tau_max": tau, "d_sample": min(d, args.cpu_sample)},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
@@ -313,7 +340,7 @@ def main():
     from paper_2604_12902_b200.workload import synthetic_c0
 
     p = MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
-    host = synthetic_c0(d, p, seed=rank)
+    host = make_c0(args.config, d, p, seed=rank)
     eng = get_engine(p, dev)
     lib = _native.load()
     src = DeviceBatch.from_arrays(host, p, dev)
@@ -432,7 +459,8 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
         "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": "u16" if w <= 16 else "u32",
-        "data": "synthetic (generator G, SURVEY §8d; seed = rank)",
+        "data": ("64 reference-sampled L=30 programs x random inputs (seed = rank)" if args.config == "paper"
+                 else "synthetic (generator G, SURVEY §8d; seed = rank)"),
         "config": {"workload": args.config, "desc": desc, "d_per_gpu": d, "w": w, "n": n,
                    "ell": ell, "s": s, "tau_max": tau, "epoch": args.epoch,
                    "machine_steps_per_gpu": machine_steps, "halted_frac": total_halted / (d * world),
