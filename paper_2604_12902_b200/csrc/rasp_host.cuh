@@ -1,0 +1,290 @@
+// rasp_host.cuh -- host-side launch machinery shared by the ABI translation
+// units: device query, tile planning, workspace layout, the epoch scheduler
+// (launch_epochs) and the template dispatch.  Instantiated per HBM word type
+// in rasp_inst_s*.cu so the kernels compile in parallel.
+#pragma once
+#include "rasp_kernels.cuh"
+#include "raspvisor_b200.h"
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+namespace rasp {
+namespace host {
+
+extern thread_local char g_cuda_err[256];
+extern std::atomic<unsigned long long> g_launches;
+
+inline int cuda_fail(cudaError_t e, const char *what)
+{
+    std::snprintf(g_cuda_err, sizeof g_cuda_err, "%s: %s", what, cudaGetErrorString(e));
+    return RASP_ECUDA;
+}
+
+#define RASP_CUDA(call)                                   \
+    do {                                                  \
+        cudaError_t e_ = (call);                          \
+        if (e_ != cudaSuccess) return cuda_fail(e_, #call); \
+    } while (0)
+
+using rasp::kMaxEpochs;                 // schedule slots in the workspace
+constexpr int kPollAfter = 24;          // epochs after which the host polls the schedule
+constexpr uint32_t kMaxK = 1u << 24;    // longest epoch, in steps
+constexpr int kWarpsPerBlockMax = 4;
+constexpr size_t kBigTile = 16 * 1024;  // tiles above this use the one-warp, many-register kernel
+constexpr size_t kGlobalTileBudget = size_t(1) << 30;  // bytes of HBM tiles for huge n
+
+struct Device {
+    int id = -1, nsm = 0, smem_optin = 0;
+};
+
+inline int device_info(Device &dv)
+{
+    int id = 0;
+    RASP_CUDA(cudaGetDevice(&id));
+    static thread_local Device cache;
+    if (cache.id != id) {
+        Device d;
+        d.id = id;
+        RASP_CUDA(cudaDeviceGetAttribute(&d.nsm, cudaDevAttrMultiProcessorCount, id));
+        RASP_CUDA(cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, id));
+        cache = d;
+    }
+    dv = cache;
+    return RASP_OK;
+}
+
+inline size_t natural_bytes(uint32_t w) { return w <= 8 ? 1 : w <= 16 ? 2 : w <= 32 ? 4 : 8; }
+inline size_t cell_bytes(uint32_t w) { return w <= 16 ? 2 : w <= 32 ? 4 : 8; }   // tile cell SC
+inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
+
+inline int check_params(const rasp_params *p)
+{
+    if (!p || p->w < 1 || p->w > 64 || p->n < 2) return RASP_EPARAM;
+    const uint64_t limit_m1 = p->w == 64 ? ~0ull : ((1ull << p->w) - 1);
+    if (p->ell < 1 || p->s < 1 || p->ell > limit_m1 || p->s > limit_m1) return RASP_EPARAM;
+    if (p->ell >= (1ull << 31) || p->s >= (1ull << 31)) return RASP_ECAPACITY;
+    return RASP_OK;
+}
+
+struct Plan {
+    bool smem = true;
+    int warps_per_block = 1;
+    int blocks = 1;
+    size_t tile_bytes = 0;
+    size_t dyn_smem = 0;
+    size_t gtile_bytes = 0;   // workspace bytes for HBM tiles (huge n only)
+};
+
+inline uint64_t tile_rows(const rasp_params *p) { return uint64_t(p->n) + p->ell + 1 + p->s; }
+
+// Sizing that does not need the kernel handle (workspace size).
+inline void plan_shape(const rasp_params *p, const Device &dv, Plan &pl)
+{
+    pl.tile_bytes = tile_rows(p) * 32 * cell_bytes(p->w);
+    if (pl.tile_bytes <= size_t(dv.smem_optin)) {
+        pl.smem = true;
+        pl.warps_per_block = int(std::min<size_t>(kWarpsPerBlockMax, dv.smem_optin / pl.tile_bytes));
+        pl.dyn_smem = pl.tile_bytes * pl.warps_per_block;
+        pl.gtile_bytes = 0;
+    } else {
+        pl.smem = false;
+        pl.warps_per_block = 1;
+        pl.dyn_smem = 0;
+        const size_t warps = std::max<size_t>(
+            dv.nsm, std::min<size_t>(size_t(dv.nsm) * 16, kGlobalTileBudget / pl.tile_bytes));
+        pl.blocks = int(warps);
+        pl.gtile_bytes = warps * pl.tile_bytes;
+    }
+}
+
+struct Workspace {
+    uint32_t *lists[2];
+    rasp::Sched *sched;
+    void *gtiles;
+};
+
+inline size_t workspace_layout(const rasp_params *p, uint64_t d, const Plan &pl, void *base, Workspace *ws)
+{
+    size_t off = 0;
+    char *b = static_cast<char *>(base);
+    const size_t list_bytes = align256(sizeof(uint32_t) * std::max<uint64_t>(d, 1));
+    if (ws) ws->lists[0] = reinterpret_cast<uint32_t *>(b + off);
+    off += list_bytes;
+    if (ws) ws->lists[1] = reinterpret_cast<uint32_t *>(b + off);
+    off += list_bytes;
+    if (ws) ws->sched = reinterpret_cast<rasp::Sched *>(b + off);
+    off += align256(sizeof(rasp::Sched));
+    if (ws) ws->gtiles = pl.gtile_bytes ? b + off : nullptr;
+    off += align256(pl.gtile_bytes);
+    (void)p;
+    return off;
+}
+
+template <class S, class SC, class CT, bool POW2, rasp::Arith AR, bool BUDGET, bool SMEM, bool BIG = false>
+int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const Workspace &ws,
+                  uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
+{
+    auto kern = rasp::epoch_kernel<S, SC, CT, POW2, AR, BUDGET, SMEM, BIG>;
+    if (SMEM) {
+        // warps per block chosen to maximise resident warps per SM (ties: more
+        // warps per block); attribute + occupancy queried once per
+        // (instantiation, device, tile size)
+        struct Cached { int dev = -1; size_t tile = 0; int wpb = 0; int per_sm = 0; };
+        static thread_local Cached c;
+        if (c.dev != dv.id || c.tile != pl.tile_bytes) {
+            int best_w = 0, best_ps = 0;
+            for (int wpb = BIG ? 1 : kWarpsPerBlockMax; wpb >= 1; --wpb) {
+                const size_t smem = pl.tile_bytes * size_t(wpb);
+                if (smem > size_t(dv.smem_optin)) continue;
+                RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+                int per_sm = 0;
+                RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
+                if (per_sm * wpb > best_ps * best_w) {
+                    best_w = wpb;
+                    best_ps = per_sm;
+                }
+            }
+            if (best_w == 0) return RASP_ECAPACITY;
+            RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           int(pl.tile_bytes * size_t(best_w))));
+            c.dev = dv.id;
+            c.tile = pl.tile_bytes;
+            c.wpb = best_w;
+            c.per_sm = best_ps;
+        }
+        pl.warps_per_block = c.wpb;
+        pl.dyn_smem = pl.tile_bytes * size_t(c.wpb);
+        pl.blocks = c.per_sm * dv.nsm;
+    }
+    const int threads = 32 * pl.warps_per_block;
+    const uint64_t tiles = (d + 31) / 32;
+    const uint64_t need_blocks = (tiles + pl.warps_per_block - 1) / pl.warps_per_block;
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(uint64_t(pl.blocks), need_blocks)));
+
+    RASP_CUDA(cudaMemsetAsync(ws.sched, 0, sizeof(rasp::Sched), st));
+    // Enough launches for the pure doubling schedule; the device schedule can
+    // only finish sooner (it lengthens epochs once survivors stop halting).
+    const uint64_t K0 = uint64_t(std::min<int64_t>(std::max<int64_t>(epoch, 1), tau_max));
+    int planned = 1;
+    bool covers = int64_t(K0) >= tau_max;
+    {
+        uint64_t cov = K0, k = std::max<uint64_t>(K0, 1);
+        while (int64_t(cov) < tau_max && planned < kPollAfter) {
+            k = std::min<uint64_t>(k * 2, kMaxK);
+            cov += k;
+            ++planned;
+        }
+        covers = int64_t(cov) >= tau_max;
+    }
+    for (int e = 0;; ++e) {
+        if (e >= kMaxEpochs) return RASP_ECAPACITY;
+        if (e >= planned && covers) break;   // fully asynchronous in the common case
+        if (e >= planned) {
+            // long budgets: ask the device whether another epoch is needed
+            uint32_t knext = 0;
+            RASP_CUDA(cudaMemcpyAsync(&knext, &ws.sched->K[e], sizeof knext, cudaMemcpyDeviceToHost, st));
+            RASP_CUDA(cudaStreamSynchronize(st));
+            if (knext == 0) break;
+        }
+        rasp::EpochArgs a = base;
+        a.sched = ws.sched;
+        a.e = uint32_t(e);
+        a.first = e == 0;
+        a.count_in = uint32_t(d);
+        a.K0 = uint32_t(K0);
+        a.kmax = kMaxK;
+        a.list_in = e == 0 ? nullptr : ws.lists[(e - 1) & 1];
+        a.list_out = ws.lists[e & 1];
+        kern<<<grid, threads, pl.dyn_smem, st>>>(a, static_cast<SC *>(ws.gtiles));
+        RASP_CUDA(cudaGetLastError());
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    return RASP_OK;
+}
+
+template <class S, class SC, class CT, bool POW2, rasp::Arith AR>
+int dispatch_budget(const rasp::EpochArgs &a, const Plan &pl, const Device &dv, const Workspace &ws,
+                    uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
+{
+    if (sizeof(SC) >= 4 && pl.tile_bytes > kBigTile) {
+        if (a.fresh) return launch_epochs<S, SC, CT, POW2, AR, false, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);
+        return launch_epochs<S, SC, CT, POW2, AR, true, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);
+    }
+    if (a.fresh) return launch_epochs<S, SC, CT, POW2, AR, false, true>(a, pl, dv, ws, d, tau_max, epoch, st);
+    return launch_epochs<S, SC, CT, POW2, AR, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);
+}
+
+// S: HBM word type, SC: tile cell type, CT: arithmetic type.
+template <class S, class SC, class CT>
+int dispatch_flags(const rasp_params *p, const rasp::EpochArgs &a, const Plan &pl, const Device &dv,
+                   const Workspace &ws, uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
+{
+    using rasp::Arith;
+    if (!pl.smem)   // huge n: tiles in HBM, generic arithmetic
+        return launch_epochs<S, SC, CT, false, Arith::W1, true, false>(a, pl, dv, ws, d, tau_max, epoch, st);
+    const bool pow2 = (p->n & (p->n - 1)) == 0;
+    if constexpr (sizeof(SC) == 2) {
+        if (p->w == 1) {
+            if (pow2) return dispatch_budget<S, SC, CT, true, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
+            return dispatch_budget<S, SC, CT, false, Arith::W1>(a, pl, dv, ws, d, tau_max, epoch, st);
+        }
+        if (p->w == 16) {
+            if (pow2) return dispatch_budget<S, SC, CT, true, Arith::CELL>(a, pl, dv, ws, d, tau_max, epoch, st);
+            return dispatch_budget<S, SC, CT, false, Arith::CELL>(a, pl, dv, ws, d, tau_max, epoch, st);
+        }
+    } else {
+        if (p->w == 8 * sizeof(CT)) {
+            if (pow2) return dispatch_budget<S, SC, CT, true, Arith::FULL>(a, pl, dv, ws, d, tau_max, epoch, st);
+            return dispatch_budget<S, SC, CT, false, Arith::FULL>(a, pl, dv, ws, d, tau_max, epoch, st);
+        }
+    }
+    if (pow2) return dispatch_budget<S, SC, CT, true, Arith::NARROW>(a, pl, dv, ws, d, tau_max, epoch, st);
+    return dispatch_budget<S, SC, CT, false, Arith::NARROW>(a, pl, dv, ws, d, tau_max, epoch, st);
+}
+
+// Device-to-device copy with a kernel (cudaMemcpyAsync D2D would occupy a copy
+// engine that host<->device pipelines need).
+inline int dev_copy(void *dst, const void *src, size_t bytes, const Device &dv, cudaStream_t st)
+{
+    if (bytes == 0) return RASP_OK;
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src);
+    const size_t n16 = (a & 15) ? 0 : bytes / 16;
+    const size_t head = n16 * 16;
+    const unsigned blocks = unsigned(std::max<size_t>(1, std::min<size_t>((n16 + 255) / 256, size_t(dv.nsm) * 8)));
+    rasp::copy_kernel<<<blocks, 256, 0, st>>>(static_cast<const uint4 *>(src), static_cast<uint4 *>(dst), n16,
+                                              static_cast<const unsigned char *>(src) + head,
+                                              static_cast<unsigned char *>(dst) + head, bytes - head);
+    RASP_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return RASP_OK;
+}
+
+inline rasp::Side side_of(const rasp_batch *b)
+{
+    rasp::Side s;
+    s.iw = b->iw; s.ac = b->ac; s.M = b->M; s.u = b->u; s.y = b->y;
+    s.status = b->status; s.steps = b->steps; s.tau_h = b->tau_h;
+    return s;
+}
+
+
+// Run dispatch for one HBM word type (definitions in rasp_inst_s<bytes>.cu).
+template <class S>
+int run_typed(const rasp_params *p, const EpochArgs &a, const Plan &pl, const Device &dv,
+              const Workspace &ws, uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st);
+#define RASP_DECL_RUN(S)                                                                         \
+    template <>                                                                                  \
+    int run_typed<S>(const rasp_params *p, const EpochArgs &a, const Plan &pl, const Device &dv, \
+                     const Workspace &ws, uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st);
+RASP_DECL_RUN(uint8_t)
+RASP_DECL_RUN(uint16_t)
+RASP_DECL_RUN(uint32_t)
+RASP_DECL_RUN(uint64_t)
+#undef RASP_DECL_RUN
+
+}  // namespace host
+}  // namespace rasp

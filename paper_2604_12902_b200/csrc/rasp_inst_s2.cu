@@ -1,0 +1,16 @@
+// rasp_inst_s2.cu -- epoch-kernel instantiations for 2-byte HBM words.
+#include "rasp_host.cuh"
+
+namespace rasp {
+namespace host {
+
+template <>
+int run_typed<uint16_t>(const rasp_params *p, const EpochArgs &a, const Plan &pl, const Device &dv,
+                   const Workspace &ws, uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
+{
+    // 2-byte words: w <= 16, u16 tile cells
+    return dispatch_flags<uint16_t, uint16_t, uint32_t>(p, a, pl, dv, ws, d, tau_max, epoch, st);
+}
+
+}  // namespace host
+}  // namespace rasp

@@ -165,11 +165,10 @@ __device__ __forceinline__ uint4 get16(const SC *col, uint32_t k)
 // Loads are issued in batches (8 x 16 B, or 8 scalars) before any of the
 // dependent shared-memory stores, so a row costs ~one DRAM latency instead
 // of one per chunk.
-template <class S, class SC>
+template <class S, class SC, uint32_t B = 8>
 __device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t ncells, SC *col)
 {
     constexpr uint32_t PER = 16 / sizeof(S);
-    constexpr uint32_t B = 8;
     uint32_t k = 0;
     if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
         const uint4 *v = reinterpret_cast<const uint4 *>(row);
@@ -390,10 +389,13 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
     }
 }
 
-template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
-__global__ void __launch_bounds__(128, SMEM ? 10 : 1)
+// BIG: tiles of more than 16 KB (few warps per SM): one-warp blocks with a
+// large register budget, so a row load keeps 32 x 16 B in flight.
+template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM, bool BIG = false>
+__global__ void __launch_bounds__(BIG ? 32 : 128, BIG ? 8 : (SMEM ? 10 : 1))
 epoch_kernel(const EpochArgs A, SC *gtiles)
 {
+    constexpr uint32_t LB = BIG ? 32 : 8;   // row-load batch
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr uint32_t ROW = 32 * sizeof(SC);
     const uint32_t lane = threadIdx.x & 31;
@@ -472,8 +474,8 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 L.a = static_cast<CT>(static_cast<const S *>(src.ac)[id]);
                 L.ua = U + static_cast<uint32_t>(srcU[0]) * ROW;
                 L.ya = Y + static_cast<uint32_t>(srcY[0]) * ROW;
-                load_row<S, SC>(srcM, n, reinterpret_cast<SC *>(gb + lm));
-                load_row<S, SC>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
+                load_row<S, SC, LB>(srcM, n, reinterpret_cast<SC *>(gb + lm));
+                load_row<S, SC, LB>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
             }
             const uint64_t rem64 = (steps0 >= A.tau_max) ? 0ull
                                                          : static_cast<uint64_t>(A.tau_max - steps0);
@@ -799,7 +801,7 @@ __global__ void generate_kernel(Side b, uint64_t d, uint64_t first, uint32_t n, 
 }
 
 // Bulk device copy on the SMs (keeps the copy engines free for host traffic).
-__global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ dst, uint64_t n16,
+static __global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ dst, uint64_t n16,
                             const unsigned char *__restrict__ srcb, unsigned char *__restrict__ dstb,
                             uint64_t tail)
 {
@@ -811,7 +813,7 @@ __global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restrict__ d
 }
 
 // 102-bucket halting histogram (hypervisor.py:326-352).
-__global__ void histogram_kernel(const int8_t *__restrict__ status, const int64_t *__restrict__ tau_h,
+static __global__ void histogram_kernel(const int8_t *__restrict__ status, const int64_t *__restrict__ tau_h,
                                  uint64_t d, unsigned long long *__restrict__ out)
 {
     __shared__ unsigned int h[102];
