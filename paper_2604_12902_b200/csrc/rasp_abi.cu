@@ -80,7 +80,7 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.tau_max = tau_max;
     a.fresh = (flags & RASP_FRESH) ? 1 : 0;
     a.inplace = (in->iw == out->iw) ? 1 : 0;
-    a.tile_rows = uint32_t(tile_rows(p));
+    a.tile_rows = pl.tile_rows;
     a.one = 1;
     a.two = 2;
     a.row = uint32_t(32 * cell_bytes(p->w));

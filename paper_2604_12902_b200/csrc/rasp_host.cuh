@@ -72,6 +72,8 @@ inline int check_params(const rasp_params *p)
 
 struct Plan {
     bool smem = true;
+    bool big = false;         // one-warp blocks, y not staged in the tile
+    uint32_t tile_rows = 0;
     int warps_per_block = 1;
     int blocks = 1;
     size_t tile_bytes = 0;
@@ -84,7 +86,13 @@ inline uint64_t tile_rows(const rasp_params *p) { return uint64_t(p->n) + p->ell
 // Sizing that does not need the kernel handle (workspace size).
 inline void plan_shape(const rasp_params *p, const Device &dv, Plan &pl)
 {
-    pl.tile_bytes = tile_rows(p) * 32 * cell_bytes(p->w);
+    pl.tile_rows = uint32_t(tile_rows(p));
+    pl.tile_bytes = uint64_t(pl.tile_rows) * 32 * cell_bytes(p->w);
+    pl.big = cell_bytes(p->w) >= 4 && pl.tile_bytes > kBigTile;
+    if (pl.big) {   // PRI writes go to HBM directly: no output rows in the tile
+        pl.tile_rows = uint32_t(uint64_t(p->n) + p->ell + 1);
+        pl.tile_bytes = uint64_t(pl.tile_rows) * 32 * cell_bytes(p->w);
+    }
     if (pl.tile_bytes <= size_t(dv.smem_optin)) {
         pl.smem = true;
         pl.warps_per_block = int(std::min<size_t>(kWarpsPerBlockMax, dv.smem_optin / pl.tile_bytes));
@@ -92,6 +100,9 @@ inline void plan_shape(const rasp_params *p, const Device &dv, Plan &pl)
         pl.gtile_bytes = 0;
     } else {
         pl.smem = false;
+        pl.big = false;
+        pl.tile_rows = uint32_t(tile_rows(p));
+        pl.tile_bytes = uint64_t(pl.tile_rows) * 32 * cell_bytes(p->w);
         pl.warps_per_block = 1;
         pl.dyn_smem = 0;
         const size_t warps = std::max<size_t>(
@@ -210,7 +221,7 @@ template <class S, class SC, class CT, bool POW2, rasp::Arith AR>
 int dispatch_budget(const rasp::EpochArgs &a, const Plan &pl, const Device &dv, const Workspace &ws,
                     uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
 {
-    if (sizeof(SC) >= 4 && pl.tile_bytes > kBigTile) {
+    if (sizeof(SC) >= 4 && pl.big) {
         if (a.fresh) return launch_epochs<S, SC, CT, POW2, AR, false, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);
         return launch_epochs<S, SC, CT, POW2, AR, true, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);
     }

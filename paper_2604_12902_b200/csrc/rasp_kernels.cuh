@@ -86,7 +86,7 @@ struct EpochArgs {
     uint32_t first;                // read the batch from `in`
     uint32_t fresh;                // status=0, steps=0, tau_h=-1 on input
     uint32_t inplace;              // in == out
-    uint32_t tile_rows;            // n + ell + 1 + s
+    uint32_t tile_rows;            // n + ell + 1 (+ s output rows unless BIG)
     uint32_t one, two;             // the constants 1 and 2 (see Opq)
     uint32_t row;                  // bytes per tile row (32 * sizeof(SC))
     uint32_t stable_q8;            // survival ratio (x256) at which the rest runs as one epoch
@@ -348,10 +348,12 @@ __device__ __forceinline__ bool is_fixed(const LaneState<CT> &L, const Fetch<CT>
 // t == K always checks it.  A lane's verdict time is the last t at which it
 // was live (tlast); whether it halted or ran out of budget is decided at
 // write-back.
-template <class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM>
+// YG (big tiles): the output tape is not staged in the tile; PRI stores go
+// straight to the machine's HBM row (ybase + ya, element type YS).
+template <class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM, bool YG = false, class YS = SC>
 __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
                                           uint32_t yend, const Geo &g, const Opq &q, uint32_t t,
-                                          bool can_apply)
+                                          bool can_apply, char *ybase = nullptr)
 {
     const CT mask = static_cast<CT>(g.mask);
     const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, base, lm, g, q);
@@ -377,8 +379,13 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
         L.ua += q.row;
     }
     if (app & (f.o == 7) & (L.ya < yend)) {
-        st_cell<SC, CT, SMEM>(base, L.ya, f.mj);
-        L.ya += q.row;
+        if constexpr (YG) {
+            *reinterpret_cast<YS *>(ybase + L.ya) = static_cast<YS>(f.mj);
+            L.ya += static_cast<uint32_t>(sizeof(YS));
+        } else {
+            st_cell<SC, CT, SMEM>(base, L.ya, f.mj);
+            L.ya += q.row;
+        }
     }
     if (app) {
         const bool taken = (f.o == 5) & ((AR == Arith::CELL ? (a0 & mask) : a0) != 0);
@@ -418,7 +425,11 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     const uint32_t tz = threadIdx.x >> 10;
     const Opq q = {A.one + tz, A.two + tz, A.row + tz};
     const uint32_t U = n * ROW + lm;                       // u[1] of this lane
-    const uint32_t Y = (n + A.g.ell + 1) * ROW + lm;       // y[1] of this lane (epoch scratch)
+    // y[1] of this lane: a tile row (epoch scratch), or (BIG) an offset from the
+    // lane's HBM output row
+    const uint32_t Y = BIG ? 0u : (n + A.g.ell + 1) * ROW + lm;
+    constexpr uint32_t YSTEP = BIG ? static_cast<uint32_t>(sizeof(S)) : ROW;
+    char *ybase = nullptr;
     // generic base for the (cold) row copies: gb + address = generic pointer
     char *gb = SMEM ? reinterpret_cast<char *>(smem_raw) -
                           static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw))
@@ -473,7 +484,8 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 L.i = static_cast<CT>(static_cast<const S *>(src.iw)[id]);
                 L.a = static_cast<CT>(static_cast<const S *>(src.ac)[id]);
                 L.ua = U + static_cast<uint32_t>(srcU[0]) * ROW;
-                L.ya = Y + static_cast<uint32_t>(srcY[0]) * ROW;
+                L.ya = Y + static_cast<uint32_t>(srcY[0]) * YSTEP;
+                if constexpr (BIG) ybase = reinterpret_cast<char *>(static_cast<S *>(A.out.y) + id * ycols + 1);
                 load_row<S, SC, LB>(srcM, n, reinterpret_cast<SC *>(gb + lm));
                 load_row<S, SC, LB>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
             }
@@ -487,20 +499,20 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
         {   // ---- step loop
             const Geo g = A.g;
             const uint32_t uend = U + g.ell * ROW;
-            const uint32_t yend = Y + g.s * ROW;
+            const uint32_t yend = Y + g.s * YSTEP;
             uint32_t t = 0;
             bool live = __any_sync(kFull, L.active);
             for (; live && t + 2 <= K; t += 2) {
-                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, q, t, true);
-                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, q, t + 1, true);
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, true, ybase);
                 live = __any_sync(kFull, L.active);
             }
             if (live && t < K) {
-                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM>(L, tb, lm, uend, yend, g, q, t, true);
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
                 ++t;
                 live = __any_sync(kFull, L.active);
             }
-            if (live) rasp_step<SC, CT, POW2, AR, true, SMEM>(L, tb, lm, uend, yend, g, q, K, false);
+            if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
         }
         if (lane == 0) next = atomicAdd(&sc->tile_ctr[e], 1u);   // overlaps the write-back
 
@@ -516,12 +528,14 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const int64_t steps0 = fresh ? covered : dst.steps[id];
             const uint32_t y0_start = static_cast<uint32_t>(static_cast<const S *>(src.y)[id * ycols]);
             const uint32_t u0 = (L.ua - U) / ROW;
-            const uint32_t y0 = (L.ya - Y) / ROW;
+            const uint32_t y0 = (L.ya - Y) / YSTEP;
             if constexpr (kRawI<POW2, AR>) L.i &= static_cast<CT>(A.g.mask);
             if constexpr (AR == Arith::CELL) L.a &= static_cast<CT>(A.g.mask);
             S *dY = static_cast<S *>(dst.y) + id * ycols;
-            const SC *colY = reinterpret_cast<const SC *>(gb + Y);
-            for (uint32_t k = y0_start; k < y0; ++k) dY[k + 1] = static_cast<S>(colY[k * 32]);
+            if constexpr (!BIG) {
+                const SC *colY = reinterpret_cast<const SC *>(gb + Y);
+                for (uint32_t k = y0_start; k < y0; ++k) dY[k + 1] = static_cast<S>(colY[k * 32]);
+            }
             dY[0] = static_cast<S>(y0);
             static_cast<S *>(dst.iw)[id] = static_cast<S>(L.i);
             static_cast<S *>(dst.ac)[id] = static_cast<S>(L.a);
@@ -531,7 +545,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 // the configuration is not a fixed point
                 bool halted = true;
                 if (L.tlast == L.rem) {
-                    const uint32_t uend = U + A.g.ell * ROW, yend = Y + A.g.s * ROW;
+                    const uint32_t uend = U + A.g.ell * ROW, yend = Y + A.g.s * YSTEP;
                     const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, tb, lm, A.g, q);
                     halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, A.g, q);
                 }
