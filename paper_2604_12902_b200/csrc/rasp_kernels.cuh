@@ -227,9 +227,9 @@ struct LaneState {
     bool active;
 };
 
-// Runtime constants held in registers.  Adding a register (rather than an
-// immediate) lets ptxas issue the add on the FMA pipe (IMAD.IADD) instead of
-// the ALU pipe, which the predicate logic of the step already saturates.
+// Step constants (1, 2, bytes per tile row).  Kept as a struct so callers
+// can pass them; they are compile-time values (runtime copies were
+// rematerialised by ptxas from the constant bank inside the loop).
 struct Opq {
     uint32_t one, two, row;
 };
@@ -422,8 +422,9 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
         lm = lane * static_cast<uint32_t>(sizeof(SC));
     }
     // per-thread copies (threadIdx.x >> 10 == 0): not uniform, so adds stay on IMAD
-    const uint32_t tz = threadIdx.x >> 10;
-    const Opq q = {A.one + tz, A.two + tz, A.row + tz};
+    // compile-time constants: ptxas rematerialises runtime ones with LDC inside
+    // the step loop, which put a constant-cache latency on the critical path
+    const Opq q = {1u, 2u, ROW};
     const uint32_t U = n * ROW + lm;                       // u[1] of this lane
     // y[1] of this lane: a tile row (epoch scratch), or (BIG) an offset from the
     // lane's HBM output row
@@ -655,7 +656,7 @@ enum_kernel(const EnumArgs A)
     SC *colM = reinterpret_cast<SC *>(gb + lm);
     const uint32_t U = n * ROW + lm, Y = (n + 2) * ROW + lm;
     const uint32_t uend = U + ROW, yend = Y + ROW;
-    const Opq q = {A.one, A.two, A.row};
+    const Opq q = {1u, 2u, ROW};
     const uint32_t pw = A.ob + A.pb;
     const uint32_t x = threadIdx.x;                 // the input word of this lane
     const bool valid_x = x <= static_cast<uint32_t>(g.mask);
