@@ -410,11 +410,13 @@ def main():
 
     # --- e2e through the public API with host buffers (pinned), copies inside
     from paper_2604_12902_b200.pipeline import HostPipeline
+    # the reference's inputs are programs and input words (build_workload ->
+    # init_config, hv:362-384): copy those in, assemble c0 on the device
     pipe = HostPipeline(p, d, dev, engine=eng)
-    pin_in = pipe.pinned_inputs(host)
+    pin_in = pipe.pinned_programs(host["M"], host["u"][:, 1:])
     e2e_times = []
     for it in range(args.warmup + args.steps):
-        t = pipe.run(pin_in, tau, args.epoch)
+        t = pipe.run_programs(pin_in, tau, args.epoch)
         if it >= args.warmup:
             e2e_times.append(t)
     t_e2e = statistics.mean(e2e_times)

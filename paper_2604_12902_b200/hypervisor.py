@@ -31,7 +31,7 @@ from .machine import Config, MachineParams, validate_config
 
 __all__ = [
     "VmStatus", "BatchConfig", "VmSlot", "SlotView", "BatchResult", "run_batch",
-    "run_arrays", "run_device", "collect_histogram", "HISTOGRAM_KEYS", "get_engine",
+    "run_arrays", "run_device", "run_programs", "collect_histogram", "HISTOGRAM_KEYS", "get_engine",
 ]
 
 _RUNNING, _HALTED, _EXHAUSTED = 0, 1, 2
@@ -195,6 +195,41 @@ def run_arrays(arrays: dict, params: MachineParams, batch: BatchConfig, device=N
     slots = SlotView(res["iw"], res["ac"], res["M"], res["u"], res["y"], res["status"],
                      res["steps"], res["tau_h"], params)
     return BatchResult(slots=slots, histogram=hist, wall_time=wall)
+
+
+def run_programs(programs, inputs, params: MachineParams, batch: BatchConfig, device=None,
+                 chunks: int = 4) -> BatchResult:
+    """build_workload -> run_batch in one call: c0(P, x) = init_config(P, x)
+    (machine.py:289-309) for every row of programs [d, L] / inputs [d, k],
+    assembled on the GPU from host buffers, run, and returned as a SlotView.
+    Same errors as init_config / run_batch (CapacityError, ValueError)."""
+    from .pipeline import HostPipeline
+    P = np.asarray(programs)
+    X = np.asarray(inputs)
+    d = int(P.shape[0])
+    X = X.reshape(d, -1) if X.size else np.zeros((d, 0), P.dtype)
+    _budget_check(d, params, batch)
+    if P.shape[1] > params.n:
+        raise CapacityError(f"program needs {P.shape[1]} memory words but n = {params.n}")
+    if X.shape[1] > params.ell:
+        raise CapacityError(f"input vector has {X.shape[1]} words but ell = {params.ell}")
+    if params.w < 64:
+        for kind, arr in (("program", P), ("input", X)):
+            if arr.size and int(arr.max()) > params.mask:
+                raise ValueError(f"{kind} word {int(arr.max())} out of range for w = {params.w}")
+    if d == 0:
+        return run_arrays({"iw": np.zeros(0, params.dtype), "ac": np.zeros(0, params.dtype),
+                           "M": np.zeros((0, params.n), params.dtype),
+                           "u": np.zeros((0, params.ell + 1), params.dtype),
+                           "y": np.zeros((0, params.s + 1), params.dtype)}, params, batch, device)
+    pipe = HostPipeline(params, d, device, chunks=chunks)
+    pinned = pipe.pinned_programs(P, X)
+    wall = pipe.run_programs(pinned, batch.tau_max, batch.epoch)
+    res = pipe.results()
+    slots = SlotView(res["iw"], res["ac"], res["M"], res["u"], res["y"], res["status"],
+                     res["steps"], res["tau_h"], params)
+    return BatchResult(slots=slots, histogram=_histogram_counter(res["status"], res["tau_h"]),
+                       wall_time=wall)
 
 
 def run_batch(configs, params: MachineParams, batch: BatchConfig, device=None) -> BatchResult:

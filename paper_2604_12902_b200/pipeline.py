@@ -91,5 +91,58 @@ class HostPipeline:
         e1.synchronize()
         return e0.elapsed_time(e1) / 1e3
 
+    # --- programs + inputs (init_config on the device) --------------------------
+    def pinned_programs(self, programs, inputs) -> dict:
+        """Pinned copies of programs [d, L] and inputs [d, k] (the arguments of
+        init_config, machine.py:289-309); c0 is assembled on the device."""
+        wd = TORCH_WORD[self.wb]
+        out = {}
+        for name, arr in (("programs", programs), ("inputs", inputs)):
+            a = np.ascontiguousarray(np.asarray(arr).astype(NUMPY_WORD[self.wb]))
+            if a.ndim == 1:
+                a = a.reshape(self.d, -1)
+            t = torch.empty(a.shape, dtype=wd, pin_memory=True)
+            t.copy_(torch.from_numpy(a))
+            out[name] = t
+        if out["programs"].shape[1] > self.params.n or out["inputs"].shape[1] > self.params.ell:
+            from .errors import CapacityError
+            raise CapacityError("programs or inputs exceed the machine geometry")
+        self._stage = {k: torch.empty(v.shape, dtype=wd, device=self.device) for k, v in out.items()}
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in out.values())
+        return out
+
+    def run_programs(self, pinned: dict, tau_max: int, epoch: int = 64) -> float:
+        """End-to-end pass from programs + inputs: per chunk, copy them in,
+        assemble c0 on the device (rasp_init_c0), run in place, copy every
+        result field out.  Returns device seconds."""
+        main = torch.cuda.current_stream(self.device)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(main)
+        for s in (self.s_in, self.s_run, self.s_out):
+            s.wait_event(e0)
+        P, X = self._stage["programs"], self._stage["inputs"]
+        for a, b in self.bounds:
+            with torch.cuda.stream(self.s_in):
+                P[a:b].copy_(pinned["programs"][a:b], non_blocking=True)
+                if X.shape[1]:
+                    X[a:b].copy_(pinned["inputs"][a:b], non_blocking=True)
+                ev_in = torch.cuda.Event()
+                ev_in.record(self.s_in)
+            self.s_run.wait_event(ev_in)
+            view = self._view(self.dev, a, b)
+            self.engine.init_c0(P[a:b], X[a:b], view, stream=self.s_run)
+            self.engine.run(view, tau_max, epoch, fresh=True, stream=self.s_run)
+            ev_run = torch.cuda.Event()
+            ev_run.record(self.s_run)
+            self.s_out.wait_event(ev_run)
+            with torch.cuda.stream(self.s_out):
+                for k in ALL_FIELDS:
+                    self.host_out[k][a:b].copy_(getattr(self.dev, k)[a:b], non_blocking=True)
+        main.wait_stream(self.s_out)
+        e1.record(main)
+        e1.synchronize()
+        return e0.elapsed_time(e1) / 1e3
+
     def results(self) -> dict:
         return {k: v.numpy() for k, v in self.host_out.items()}

@@ -274,3 +274,22 @@ def test_scalar_path_through_kernel(pkg):
     assert seen == [(0, 0), (1, 2), (2, 4)] and tau == 2 and cf.M[6] == 5
     assert scalar.run_to_fixpoint(c0, 1, p)[1] is None
     assert scalar.run_to_fixpoint(c0, 2, p)[1] == 2
+
+
+def test_run_programs_host_path(pkg):
+    """Programs + inputs from host buffers (device-side init_config, chunked
+    pipeline) give the same results as run_arrays on the assembled c0."""
+    P, H = pkg
+    p = P.MachineParams(w=16, n=64, ell=8, s=8, mu=1)
+    c0 = P.synthetic_c0(50000, p, seed=5)
+    a = H.run_programs(c0["M"], c0["u"][:, 1:], p, H.BatchConfig(tau_max=1024), chunks=3)
+    b = H.run_arrays(c0, p, H.BatchConfig(tau_max=1024))
+    for k in RESULTS:
+        np.testing.assert_array_equal(getattr(a.slots, k), getattr(b.slots, k), err_msg=k)
+    assert a.histogram == b.histogram
+    with pytest.raises(P.CapacityError):
+        H.run_programs(np.zeros((4, 66), np.uint16), np.zeros((4, 1), np.uint16), p,
+                       H.BatchConfig(tau_max=1))
+    with pytest.raises(ValueError):
+        H.run_programs(np.full((4, 2), 70000, np.uint32), np.zeros((4, 1), np.uint32), p,
+                       H.BatchConfig(tau_max=1))
