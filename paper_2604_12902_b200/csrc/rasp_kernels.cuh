@@ -225,7 +225,6 @@ struct LaneState {
     uint32_t rem;     // remaining budget at epoch start (clamped)
     uint32_t tlast;   // last local time at which the lane was still live
     bool active;
-    CT po, pj;        // speculative kernels: the instruction pair (o, j) at i, prefetched
 };
 
 // Step constants (1, 2, bytes per tile row).  Kept as a struct so callers
@@ -399,76 +398,6 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
 
 // BIG: tiles of more than 16 KB (few warps per SM): one-warp blocks with a
 // large register budget, so a row load keeps 32 x 16 B in flight.
-// Speculative step (big tiles: few warps per SM, so each step's dependent
-// chain is exposed).  The pair (o, j) at i is already in registers; while
-// this step decodes, the pairs it can move to are fetched -- the fall-through
-// pair at i+2 and the branch-target pair at j (whose opcode is M[j mod n],
-// i.e. the operand value mj the step loads anyway) -- and the step's own
-// store (STO/RD to M[j mod n]) is forwarded into them.  The next step then
-// starts without waiting on a load of its own opcode.  Same semantics as
-// rasp_step (only w >= 2, so is_fixed uses the short form).
-template <class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM, class YS>
-__device__ __forceinline__ void rasp_step_spec(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
-                                               uint32_t yend, const Geo &g, uint32_t t, bool can_apply,
-                                               char *ybase)
-{
-    constexpr uint32_t SH = sizeof(SC) == 2 ? 6 : sizeof(SC) == 4 ? 7 : 8;
-    const CT mask = static_cast<CT>(g.mask);
-    const Opq q = {1u, 2u, 1u << SH};
-    Fetch<CT> f;
-    f.o = L.po;
-    f.jw = L.pj;
-    const uint32_t jn = modn<CT, POW2>(f.jw, g);
-    f.jo = (jn << SH) + lm;
-    uint32_t ia2, ib2, jt1;
-    if constexpr (POW2 && AR != Arith::FULL) {      // i may be raw: reduce with (mask & (n-1))
-        ia2 = static_cast<uint32_t>(L.i + 2) & g.jm;
-        ib2 = static_cast<uint32_t>(L.i + 3) & g.jm;
-        jt1 = static_cast<uint32_t>(f.jw + 1) & g.jm;
-    } else {
-        ia2 = modn<CT, POW2>(wrap<CT, AR>(L.i + 2, mask), g);
-        ib2 = modn<CT, POW2>(wrap<CT, AR>(L.i + 3, mask), g);
-        jt1 = modn<CT, POW2>(wrap<CT, AR>(f.jw + 1, mask), g);
-    }
-    f.mj = ld_cell<SC, CT, SMEM>(base, f.jo);
-    const CT mj1 = ld_cell<SC, CT, SMEM>(base, (jt1 << SH) + lm);
-    const CT of = ld_cell<SC, CT, SMEM>(base, (ia2 << SH) + lm);
-    const CT jf = ld_cell<SC, CT, SMEM>(base, (ib2 << SH) + lm);
-    f.ud = ld_cell<SC, CT, SMEM>(base, L.ua);
-    const CT a0 = L.a;
-    const bool fixed = is_fixed<CT, POW2, AR>(L, f, uend, yend, g, q);
-    if (L.active) L.tlast = t;
-    if (BUDGET || !can_apply) L.active = L.active & !(fixed | (t == L.rem));
-    else L.active = L.active & !fixed;
-    const bool app = L.active & can_apply;
-    if (app & (f.o == 1)) L.a = f.jw;
-    if (app & (f.o == 2)) L.a = wrap<CT, AR>(a0 + f.mj, mask);
-    if (app & (f.o == 3)) L.a = wrap<CT, AR>(a0 * f.mj, mask);
-    const bool rd = (f.o == 6) & (L.ua < uend);
-    const bool sto = app & (f.o == 4);
-    const bool rda = app & rd;
-    const CT stv = sto ? a0 : f.ud;
-    if (sto | rda) st_cell<SC, CT, SMEM>(base, f.jo, stv);
-    if (rda) L.ua += q.row;
-    if (app & (f.o == 7) & (L.ya < yend)) {
-        *reinterpret_cast<YS *>(ybase + L.ya) = static_cast<YS>(f.mj);
-        L.ya += static_cast<uint32_t>(sizeof(YS));
-    }
-    if (app) {
-        const bool taken = (f.o == 5) & (a0 != 0);
-        const bool wr = sto | rda;
-        // fall-through pair with this step's store forwarded (no store on BNZ)
-        const CT nof = (wr & (jn == ia2)) ? stv : of;
-        const CT njf = (wr & (jn == ib2)) ? stv : jf;
-        L.po = taken ? f.mj : nof;
-        L.pj = taken ? mj1 : njf;
-        CT i2;
-        if constexpr (kRawI<POW2, AR>) i2 = L.i + static_cast<CT>(q.two);
-        else i2 = wrap<CT, AR>(L.i + 2, mask);
-        L.i = taken ? f.jw : i2;
-    }
-}
-
 template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM, bool BIG = false>
 __global__ void __launch_bounds__(BIG ? 32 : 128, BIG ? 8 : (SMEM ? 10 : 1))
 epoch_kernel(const EpochArgs A, SC *gtiles)
@@ -574,36 +503,17 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const uint32_t yend = Y + g.s * YSTEP;
             uint32_t t = 0;
             bool live = __any_sync(kFull, L.active);
-            if constexpr (BIG) {
-                {   // prefetch the first instruction pair
-                    const Fetch<CT> f0 = fetch<SC, CT, POW2, AR, SMEM>(L, tb, lm, g, q);
-                    L.po = f0.o;
-                    L.pj = f0.jw;
-                }
-                for (; live && t + 2 <= K; t += 2) {
-                    rasp_step_spec<SC, CT, POW2, AR, BUDGET, SMEM, S>(L, tb, lm, uend, yend, g, t, true, ybase);
-                    rasp_step_spec<SC, CT, POW2, AR, BUDGET, SMEM, S>(L, tb, lm, uend, yend, g, t + 1, true, ybase);
-                    live = __any_sync(kFull, L.active);
-                }
-                if (live && t < K) {
-                    rasp_step_spec<SC, CT, POW2, AR, BUDGET, SMEM, S>(L, tb, lm, uend, yend, g, t, true, ybase);
-                    ++t;
-                    live = __any_sync(kFull, L.active);
-                }
-                if (live) rasp_step_spec<SC, CT, POW2, AR, true, SMEM, S>(L, tb, lm, uend, yend, g, K, false, ybase);
-            } else {
-                for (; live && t + 2 <= K; t += 2) {
-                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
-                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, true, ybase);
-                    live = __any_sync(kFull, L.active);
-                }
-                if (live && t < K) {
-                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
-                    ++t;
-                    live = __any_sync(kFull, L.active);
-                }
-                if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
+            for (; live && t + 2 <= K; t += 2) {
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, true, ybase);
+                live = __any_sync(kFull, L.active);
             }
+            if (live && t < K) {
+                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
+                ++t;
+                live = __any_sync(kFull, L.active);
+            }
+            if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
         }
         if (lane == 0) next = atomicAdd(&sc->tile_ctr[e], 1u);   // overlaps the write-back
 
