@@ -18,7 +18,7 @@ from .machine import MachineParams
 
 
 class HostPipeline:
-    def __init__(self, params: MachineParams, d: int, device=None, chunks: int = 4,
+    def __init__(self, params: MachineParams, d: int, device=None, chunks: int = 8,
                  engine: Engine | None = None, word_bytes: int | None = None):
         self.params = params
         self.d = d
