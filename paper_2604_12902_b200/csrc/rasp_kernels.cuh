@@ -398,6 +398,60 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
 
 // BIG: tiles of more than 16 KB (few warps per SM): one-warp blocks with a
 // large register budget, so a row load keeps 32 x 16 B in flight.
+// Ungated step, for loop steps of runs whose machines share one budget
+// (every lane has rem >= K, so no lane can run out of budget inside the
+// loop).  A lane is then either live and not fixed -- the step applies -- or
+// sits at a fixed point, where applying the step changes nothing (that is
+// what fixed means: Φ(c) = c, hv:115).  So the update is applied to every
+// lane without an "applies" predicate: it only has to honour the cases that
+// leave i in place (opcode outside 1..7, RD at capacity) and never store in
+// them.  This takes the live/fixed bookkeeping off the update chain.
+template <class SC, class CT, bool POW2, Arith AR, bool SMEM, bool YG = false, class YS = SC>
+__device__ __forceinline__ void rasp_step_free(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
+                                               uint32_t yend, const Geo &g, const Opq &q, uint32_t t,
+                                               char *ybase = nullptr)
+{
+    static_assert(AR != Arith::W1, "w = 1 uses the gated step");
+    const CT mask = static_cast<CT>(g.mask);
+    const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, base, lm, g, q);
+    const CT a0 = L.a;
+    const bool ucap = L.ua >= uend;
+    const bool taken = (f.o == 5) & ((AR == Arith::CELL ? (a0 & mask) : a0) != 0);
+    bool self;
+    if constexpr (kRawI<POW2, AR> && AR != Arith::FULL) self = ((L.i ^ f.jw) & mask) == 0;
+    else self = f.jw == L.i;
+    const bool stay = (static_cast<CT>(f.o - 1) > 6) | ((f.o == 6) & ucap);   // i does not move
+    const bool fixed = stay | (taken & self);
+    if (L.active) L.tlast = t;
+    L.active = L.active & !fixed;
+    if (f.o == 1) L.a = f.jw;
+    if constexpr (AR == Arith::CELL) {
+        if (f.o == 2) L.a = a0 + f.mj;
+        if (f.o == 3) L.a = a0 * f.mj;
+    } else {
+        if (f.o == 2) L.a = wrap<CT, AR>(a0 + f.mj, mask);
+        if (f.o == 3) L.a = wrap<CT, AR>(a0 * f.mj, mask);
+    }
+    if (f.o == 4) st_cell<SC, CT, SMEM>(base, f.jo, a0);
+    if ((f.o == 6) & !ucap) {
+        st_cell<SC, CT, SMEM>(base, f.jo, f.ud);
+        L.ua += q.row;
+    }
+    if constexpr (YG) {   // HBM row: lanes without a machine (no ybase) must not store
+        if (L.active & (f.o == 7) & (L.ya < yend)) {
+            *reinterpret_cast<YS *>(ybase + L.ya) = static_cast<YS>(f.mj);
+            L.ya += static_cast<uint32_t>(sizeof(YS));
+        }
+    } else if ((f.o == 7) & (L.ya < yend)) {
+        st_cell<SC, CT, SMEM>(base, L.ya, f.mj);
+        L.ya += q.row;
+    }
+    CT i2;
+    if constexpr (kRawI<POW2, AR>) i2 = L.i + static_cast<CT>(q.two);
+    else i2 = wrap<CT, AR>(L.i + 2, mask);
+    L.i = taken ? f.jw : (stay ? L.i : i2);
+}
+
 template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM, bool BIG = false>
 __global__ void __launch_bounds__(BIG ? 32 : 128, BIG ? 8 : (SMEM ? 10 : 1))
 epoch_kernel(const EpochArgs A, SC *gtiles)
@@ -503,15 +557,28 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const uint32_t yend = Y + g.s * YSTEP;
             uint32_t t = 0;
             bool live = __any_sync(kFull, L.active);
-            for (; live && t + 2 <= K; t += 2) {
-                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
-                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, true, ybase);
-                live = __any_sync(kFull, L.active);
-            }
-            if (live && t < K) {
-                rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
-                ++t;
-                live = __any_sync(kFull, L.active);
+            if constexpr (!BUDGET && AR != Arith::W1) {
+                for (; live && t + 2 <= K; t += 2) {
+                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, ybase);
+                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, ybase);
+                    live = __any_sync(kFull, L.active);
+                }
+                if (live && t < K) {
+                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, ybase);
+                    ++t;
+                    live = __any_sync(kFull, L.active);
+                }
+            } else {
+                for (; live && t + 2 <= K; t += 2) {
+                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
+                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, true, ybase);
+                    live = __any_sync(kFull, L.active);
+                }
+                if (live && t < K) {
+                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
+                    ++t;
+                    live = __any_sync(kFull, L.active);
+                }
             }
             if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
         }
