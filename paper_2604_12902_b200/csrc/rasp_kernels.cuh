@@ -420,7 +420,7 @@ __device__ __forceinline__ void rasp_step_free(LaneState<CT> &L, char *base, uin
     bool self;
     if constexpr (kRawI<POW2, AR> && AR != Arith::FULL) self = ((L.i ^ f.jw) & mask) == 0;
     else self = f.jw == L.i;
-    const bool stay = (static_cast<CT>(f.o - static_cast<CT>(q.one)) > 6) | ((f.o == 6) & ucap);   // i stays
+    const bool stay = (static_cast<CT>(f.o - 1) > 6) | ((f.o == 6) & ucap);   // i does not move
     const bool fixed = stay | (taken & self);
     if (L.active) L.tlast = t;
     L.active = L.active & !fixed;
@@ -476,16 +476,9 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
         lm = lane * static_cast<uint32_t>(sizeof(SC));
     }
     // per-thread copies (threadIdx.x >> 10 == 0): not uniform, so adds stay on IMAD
-    // The step's additive constants live in registers whose value ptxas cannot
-    // see (1 read back from shared memory): register-register adds may issue on
-    // the FMA pipe (IMAD.IADD) while immediate adds are ALU-only (VIADD), and
-    // the ALU pipe is the step's bottleneck.  (Kernel parameters do not work:
-    // ptxas rematerialises them with LDC inside the loop.)
-    __shared__ uint32_t s_one;
-    if (threadIdx.x == 0) s_one = 1u;
-    __syncthreads();
-    const uint32_t one = *static_cast<volatile uint32_t *>(&s_one);   // a per-lane register holding 1
-    const Opq q = {one, 2u * one, ROW * one};
+    // compile-time constants: ptxas rematerialises runtime ones with LDC inside
+    // the step loop, which put a constant-cache latency on the critical path
+    const Opq q = {1u, 2u, ROW};
     const uint32_t U = n * ROW + lm;                       // u[1] of this lane
     // y[1] of this lane: a tile row (epoch scratch), or (BIG) an offset from the
     // lane's HBM output row
