@@ -91,10 +91,13 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
         // out-of-place: the input tapes and the bookkeeping arrays move in bulk;
         // the kernels then treat `out` as the working copy
         const size_t ub = size_t(d) * (p->ell + 1) * wb, yb = size_t(d) * (p->s + 1) * wb;
-        int rc2 = dev_copy(out->u, in->u, ub, dv, st);
-        if (!rc2) rc2 = dev_copy(out->y, in->y, yb, dv, st);
-        if (!rc2 && !a.fresh) {
-            rc2 = dev_copy(out->status, in->status, size_t(d), dv, st);
+        // fresh runs: the first epoch carries u/y rows over itself (one pass);
+        // otherwise copy the tapes and the bookkeeping arrays in bulk first
+        int rc2 = 0;
+        if (!a.fresh) {
+            rc2 = dev_copy(out->u, in->u, ub, dv, st);
+            if (!rc2) rc2 = dev_copy(out->y, in->y, yb, dv, st);
+            if (!rc2) rc2 = dev_copy(out->status, in->status, size_t(d), dv, st);
             if (!rc2) rc2 = dev_copy(out->steps, in->steps, size_t(d) * 8, dv, st);
             if (!rc2) rc2 = dev_copy(out->tau_h, in->tau_h, size_t(d) * 8, dv, st);
         }
@@ -221,7 +224,7 @@ int rasp_histogram(const int8_t *status, const int64_t *tau_h, uint64_t d, int64
     Device dv;
     int rc = device_info(dv);
     if (rc) return rc;
-    const uint64_t blocks = std::min<uint64_t>((d + 255) / 256, uint64_t(dv.nsm) * 8);
+    const uint64_t blocks = std::min<uint64_t>((d + 255) / 256, uint64_t(dv.nsm) * 2);
     rasp::histogram_kernel<<<unsigned(blocks), 256, 0, st>>>(
         status, tau_h, d, reinterpret_cast<unsigned long long *>(out));
     RASP_CUDA(cudaGetLastError());

@@ -498,6 +498,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     const uint32_t ntiles = (K == 0 && !A.first) ? 0 : (count + 31) / 32;
     if (ntiles == 0) return;   // schedule finished: K[e+1] stays 0 from the memset
     const bool copy_side = A.first && !A.inplace;
+    const bool copy_rows = copy_side && fresh;   // out-of-place fresh: this pass writes u/y rows
     const bool fresh = A.fresh != 0;
 
     uint32_t next = 0;   // lane 0: the tile this warp takes next
@@ -543,6 +544,13 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 if constexpr (BIG) ybase = reinterpret_cast<char *>(static_cast<S *>(A.out.y) + id * ycols + 1);
                 load_row<S, SC, LB>(srcM, n, reinterpret_cast<SC *>(gb + lm));
                 load_row<S, SC, LB>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
+                if (copy_rows) {   // the host skipped the bulk u/y copy: carry the tapes over here
+                    S *dU = static_cast<S *>(dst.u) + id * ucols;
+                    S *dYr = static_cast<S *>(dst.y) + id * ycols;
+                    const SC *cu = reinterpret_cast<const SC *>(gb + U);
+                    for (uint32_t k = 0; k < A.g.ell; ++k) dU[k + 1] = static_cast<S>(cu[k * 32]);
+                    for (uint32_t k = 1; k < ycols; ++k) dYr[k] = srcY[k];
+                }
             }
             const uint64_t rem64 = (steps0 >= A.tau_max) ? 0ull
                                                          : static_cast<uint64_t>(A.tau_max - steps0);
@@ -895,25 +903,34 @@ static __global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restr
 }
 
 // 102-bucket halting histogram (hypervisor.py:326-352).
-static __global__ void histogram_kernel(const int8_t *__restrict__ status, const int64_t *__restrict__ tau_h,
-                                 uint64_t d, unsigned long long *__restrict__ out)
+static __global__ void __launch_bounds__(256) histogram_kernel(const int8_t *__restrict__ status,
+                                                               const int64_t *__restrict__ tau_h, uint64_t d,
+                                                               unsigned long long *__restrict__ out)
 {
-    __shared__ unsigned int h[102];
-    for (int k = threadIdx.x; k < 102; k += blockDim.x) h[k] = 0;
+    // one private sub-histogram per warp (low smem-atomic contention), then a
+    // block reduction and one global atomic per non-empty bucket
+    constexpr int B = 102, W = 8;
+    __shared__ unsigned int h[W][B + 2];
+    const int wid = threadIdx.x >> 5;
+    for (int k = threadIdx.x; k < W * (B + 2); k += blockDim.x) (&h[0][0])[k] = 0;
     __syncthreads();
     for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < d;
          j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const int8_t st = status[j];
         if (st == kHalted) {
             const int64_t t = tau_h[j];
-            atomicAdd(&h[t < 100 ? static_cast<int>(t) : 100], 1u);
+            atomicAdd(&h[wid][t < 100 ? static_cast<int>(t) : 100], 1u);
         } else if (st == kExhausted) {
-            atomicAdd(&h[101], 1u);
+            atomicAdd(&h[wid][101], 1u);
         }
     }
     __syncthreads();
-    for (int k = threadIdx.x; k < 102; k += blockDim.x)
-        if (h[k]) atomicAdd(&out[k], static_cast<unsigned long long>(h[k]));
+    for (int k = threadIdx.x; k < B; k += blockDim.x) {
+        unsigned int v = 0;
+#pragma unroll
+        for (int w = 0; w < W; ++w) v += h[w][k];
+        if (v) atomicAdd(&out[k], static_cast<unsigned long long>(v));
+    }
 }
 
 // Word-range and cursor-range validation (m:324-327, hv:285-290).
