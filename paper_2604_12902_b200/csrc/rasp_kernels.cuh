@@ -498,8 +498,8 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     const uint32_t ntiles = (K == 0 && !A.first) ? 0 : (count + 31) / 32;
     if (ntiles == 0) return;   // schedule finished: K[e+1] stays 0 from the memset
     const bool copy_side = A.first && !A.inplace;
-    const bool copy_rows = copy_side && fresh;   // out-of-place fresh: this pass writes u/y rows
     const bool fresh = A.fresh != 0;
+    const bool copy_rows = copy_side && fresh;   // out-of-place fresh: this pass writes u/y rows
 
     uint32_t next = 0;   // lane 0: the tile this warp takes next
     if (lane == 0) next = atomicAdd(&sc->tile_ctr[e], 1u);
