@@ -91,13 +91,10 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
         // out-of-place: the input tapes and the bookkeeping arrays move in bulk;
         // the kernels then treat `out` as the working copy
         const size_t ub = size_t(d) * (p->ell + 1) * wb, yb = size_t(d) * (p->s + 1) * wb;
-        // fresh runs: the first epoch carries u/y rows over itself (one pass);
-        // otherwise copy the tapes and the bookkeeping arrays in bulk first
-        int rc2 = 0;
-        if (!a.fresh) {
-            rc2 = dev_copy(out->u, in->u, ub, dv, st);
-            if (!rc2) rc2 = dev_copy(out->y, in->y, yb, dv, st);
-            if (!rc2) rc2 = dev_copy(out->status, in->status, size_t(d), dv, st);
+        int rc2 = dev_copy(out->u, in->u, ub, dv, st);
+        if (!rc2) rc2 = dev_copy(out->y, in->y, yb, dv, st);
+        if (!rc2 && !a.fresh) {
+            rc2 = dev_copy(out->status, in->status, size_t(d), dv, st);
             if (!rc2) rc2 = dev_copy(out->steps, in->steps, size_t(d) * 8, dv, st);
             if (!rc2) rc2 = dev_copy(out->tau_h, in->tau_h, size_t(d) * 8, dv, st);
         }

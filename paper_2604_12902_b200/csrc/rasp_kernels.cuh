@@ -499,7 +499,6 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     if (ntiles == 0) return;   // schedule finished: K[e+1] stays 0 from the memset
     const bool copy_side = A.first && !A.inplace;
     const bool fresh = A.fresh != 0;
-    const bool copy_rows = copy_side && fresh;   // out-of-place fresh: this pass writes u/y rows
 
     uint32_t next = 0;   // lane 0: the tile this warp takes next
     if (lane == 0) next = atomicAdd(&sc->tile_ctr[e], 1u);
@@ -544,13 +543,6 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 if constexpr (BIG) ybase = reinterpret_cast<char *>(static_cast<S *>(A.out.y) + id * ycols + 1);
                 load_row<S, SC, LB>(srcM, n, reinterpret_cast<SC *>(gb + lm));
                 load_row<S, SC, LB>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
-                if (copy_rows) {   // the host skipped the bulk u/y copy: carry the tapes over here
-                    S *dU = static_cast<S *>(dst.u) + id * ucols;
-                    S *dYr = static_cast<S *>(dst.y) + id * ycols;
-                    const SC *cu = reinterpret_cast<const SC *>(gb + U);
-                    for (uint32_t k = 0; k < A.g.ell; ++k) dU[k + 1] = static_cast<S>(cu[k * 32]);
-                    for (uint32_t k = 1; k < ycols; ++k) dYr[k] = srcY[k];
-                }
             }
             const uint64_t rem64 = (steps0 >= A.tau_max) ? 0ull
                                                          : static_cast<uint64_t>(A.tau_max - steps0);
