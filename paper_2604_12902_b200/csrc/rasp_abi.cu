@@ -221,8 +221,8 @@ int rasp_histogram(const int8_t *status, const int64_t *tau_h, uint64_t d, int64
     Device dv;
     int rc = device_info(dv);
     if (rc) return rc;
-    const uint64_t blocks = std::min<uint64_t>((d + 255) / 256, uint64_t(dv.nsm) * 2);
-    rasp::histogram_kernel<<<unsigned(blocks), 256, 0, st>>>(
+    const uint64_t blocks = std::min<uint64_t>((d + 1023) / 1024, uint64_t(dv.nsm));
+    rasp::histogram_kernel<<<unsigned(blocks), 1024, 0, st>>>(
         status, tau_h, d, reinterpret_cast<unsigned long long *>(out));
     RASP_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);

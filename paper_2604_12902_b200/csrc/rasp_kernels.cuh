@@ -895,31 +895,38 @@ static __global__ void copy_kernel(const uint4 *__restrict__ src, uint4 *__restr
 }
 
 // 102-bucket halting histogram (hypervisor.py:326-352).
-static __global__ void __launch_bounds__(256) histogram_kernel(const int8_t *__restrict__ status,
-                                                               const int64_t *__restrict__ tau_h, uint64_t d,
-                                                               unsigned long long *__restrict__ out)
+static __global__ void __launch_bounds__(1024) histogram_kernel(const int8_t *__restrict__ status,
+                                                                const int64_t *__restrict__ tau_h, uint64_t d,
+                                                                unsigned long long *__restrict__ out)
 {
-    // one private sub-histogram per warp (low smem-atomic contention), then a
-    // block reduction and one global atomic per non-empty bucket
-    constexpr int B = 102, W = 8;
+    // one private sub-histogram per warp (low smem-atomic contention), four
+    // independent loads in flight per thread, then a block reduction and one
+    // global atomic per non-empty bucket (grid = one block per SM)
+    constexpr int B = 102, W = 32, U = 4;
     __shared__ unsigned int h[W][B + 2];
     const int wid = threadIdx.x >> 5;
     for (int k = threadIdx.x; k < W * (B + 2); k += blockDim.x) (&h[0][0])[k] = 0;
     __syncthreads();
-    for (uint64_t j = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j < d;
-         j += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const int8_t st = status[j];
-        if (st == kHalted) {
-            const int64_t t = tau_h[j];
-            atomicAdd(&h[wid][t < 100 ? static_cast<int>(t) : 100], 1u);
-        } else if (st == kExhausted) {
-            atomicAdd(&h[wid][101], 1u);
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t j0 = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; j0 < d; j0 += U * stride) {
+        int8_t st[U];
+        int64_t th[U];
+#pragma unroll
+        for (int r = 0; r < U; ++r) {
+            const uint64_t j = j0 + r * stride;
+            st[r] = j < d ? status[j] : kRunning;
+            th[r] = (j < d && st[r] == kHalted) ? tau_h[j] : 0;
+        }
+#pragma unroll
+        for (int r = 0; r < U; ++r) {
+            if (st[r] == kHalted) atomicAdd(&h[wid][th[r] < 100 ? static_cast<int>(th[r]) : 100], 1u);
+            else if (st[r] == kExhausted) atomicAdd(&h[wid][101], 1u);
         }
     }
     __syncthreads();
     for (int k = threadIdx.x; k < B; k += blockDim.x) {
         unsigned int v = 0;
-#pragma unroll
+#pragma unroll 8
         for (int w = 0; w < W; ++w) v += h[w][k];
         if (v) atomicAdd(&out[k], static_cast<unsigned long long>(v));
     }
