@@ -159,7 +159,7 @@ def cpu_reference(cfg_name, steps_k, warmup, sample_d=None, seed=0):
     times, steps_total = [], 0
     if cfg_name == "c4":
         from paper_2604_12902_b200.enumeration import C4
-        sample = min(d, (sample_d or (1 << 16)) // 4)
+        sample = min(d, (sample_d or (1 << 20)) // 4)
         for it in range(warmup + steps_k):
             t0 = time.perf_counter()
             _, steps_total = oracle.enumerate_records(C4.m, C4.opcode_bits, C4.operand_bits, C4.w,
@@ -172,7 +172,7 @@ def cpu_reference(cfg_name, steps_k, warmup, sample_d=None, seed=0):
                 "kind": "port", "sample": f"programs [0, {sample}) of the C4 domain x 256 inputs, "
                 f"{steps_total} machine-steps, {cores} threads, best of {len(times)}",
                 "seconds": best}
-    sample = min(d, sample_d or (1 << 16))
+    sample = min(d, sample_d or (1 << 20))
     p = MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
     c0 = make_c0(cfg_name, sample, p, seed)
     for it in range(warmup + steps_k):
@@ -286,7 +286,9 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--epoch", type=int, default=64)   # BatchConfig.epoch default (hv:170)
-    ap.add_argument("--cpu-sample", type=int, default=1 << 16)
+    # machines in the CPU baseline's sample: the whole batch up to 2^20 (c2, c5 and
+    # paper run in full; c3 runs 2^20 of its 16M; c4 runs 2^18 programs)
+    ap.add_argument("--cpu-sample", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
 
