@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RASP_ABI_VERSION 1
+#define RASP_ABI_VERSION 2
 
 /* error codes */
 #define RASP_OK 0
@@ -40,6 +40,7 @@ extern "C" {
 #define RASP_ECUDA -3       /* a CUDA call failed; see rasp_last_cuda_error */
 #define RASP_EWORKSPACE -4  /* workspace too small */
 #define RASP_EDTYPE -5      /* word_bytes not in {1,2,4,8} or narrower than w */
+#define RASP_ENCCL -6       /* NCCL missing or an NCCL call failed; see rasp_last_cuda_error */
 
 /* VM status codes: hypervisor.py:63-69 */
 #define RASP_RUNNING 0
@@ -144,6 +145,47 @@ int rasp_histogram(const int8_t *status, const int64_t *tau_h, uint64_t d,
  *   out[0..4] = count of words > 2^w-1 in iw, ac, M, u, y;
  *   out[5] = count of u[.][0] > ell;  out[6] = count of y[.][0] > s;  out[7] = 0. */
 int rasp_validate(const rasp_params *p, const rasp_batch *b, int64_t *out, void *stream);
+
+/* Word-width conversion between the reference's uint64 arrays and the
+ * engine's natural-width arrays (the packing step of run_batch,
+ * hypervisor.py:280-284, and its inverse when results are read back as
+ * uint64).  Converts iw, ac, M, u, y from src->word_bytes to dst->word_bytes
+ * (narrowing truncates: validate first with rasp_validate); status, steps and
+ * tau_h are copied when both batches carry them at different addresses.
+ * dst->word_bytes must hold w bits.  rasp_pack and rasp_unpack are the same
+ * operation, named for the two directions a caller uses them in. */
+int rasp_pack(const rasp_params *p, const rasp_batch *src, const rasp_batch *dst, void *stream);
+int rasp_unpack(const rasp_params *p, const rasp_batch *src, const rasp_batch *dst, void *stream);
+
+/* The k longest halting runs, for bb-search's report (cli.py:195-230): among
+ * machines with status HALTED, the k largest tau_h, ties broken by the lower
+ * machine index, in the order of sorted(best, reverse=True) over the
+ * reference's (tau_h, -index) heap.  out_index/out_tau: int64[k] device
+ * buffers; entries past the number of halted machines are -1.  tau_max bounds
+ * every halted tau_h (rasp_run's contract) and sets the radix-select depth.
+ * k <= 2048.  workspace: device buffer of rasp_topk_workspace_bytes(k). */
+size_t rasp_topk_workspace_bytes(uint32_t k);
+int rasp_topk(const int8_t *status, const int64_t *tau_h, uint64_t d, int64_t tau_max, uint32_t k,
+              int64_t *out_index, int64_t *out_tau, void *workspace, size_t workspace_bytes, void *stream);
+
+/* Post-run collectives of a sharded run on an NCCL
+ * communicator (ncclComm_t passed as void*).  NCCL is resolved at run time from
+ * the process (the libnccl.so.2 torch loaded) or $RASP_NCCL_LIBRARY.
+ * Shard k of a d_total-machine batch over W ranks is the contiguous block
+ * [k*ceil(d_total/W), (k+1)*ceil(d_total/W)) clipped to d_total. */
+int rasp_nccl_unique_id(void *id_out /* 128 bytes */);
+int rasp_nccl_comm_init(int nranks, const void *id, int rank, void **comm_out);
+int rasp_nccl_comm_destroy(void *comm);
+/* In-place sum over ranks of `count` int64 device counters (the 102-bucket
+ * histogram plus whatever totals the caller appends). */
+int rasp_shard_allreduce(void *comm, int64_t *counters, uint64_t count, void *stream);
+/* Gather every rank's shard fields into `full` (d_total machines) on `root`;
+ * `full` is ignored on other ranks.  fields: a mask of RASP_GATHER_*. */
+#define RASP_GATHER_RESULTS 1u   /* status, steps, tau_h */
+#define RASP_GATHER_OUTPUT 2u    /* y */
+#define RASP_GATHER_CONFIG 4u    /* iw, ac, M, u */
+int rasp_shard_gather(void *comm, int root, const rasp_params *p, uint64_t d_total, const rasp_batch *shard,
+                      const rasp_batch *full, uint32_t fields, void *stream);
 
 /* Text for a RASP_E* code, and the last CUDA error string seen by this library. */
 const char *rasp_error_string(int code);

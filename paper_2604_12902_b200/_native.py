@@ -15,14 +15,21 @@ from .errors import NativeError
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libraspvisor_b200.so")
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 RASP_FRESH = 1
 
 # symbols declared by include/raspvisor_b200.h
 EXPORTS = ("rasp_workspace_bytes", "rasp_run", "rasp_histogram", "rasp_validate",
            "rasp_error_string", "rasp_last_cuda_error", "rasp_abi_version",
-           "rasp_launch_count", "rasp_enumerate", "rasp_init_c0", "rasp_generate")
+           "rasp_launch_count", "rasp_enumerate", "rasp_init_c0", "rasp_generate",
+           "rasp_pack", "rasp_unpack", "rasp_topk_workspace_bytes", "rasp_topk",
+           "rasp_nccl_unique_id", "rasp_nccl_comm_init", "rasp_nccl_comm_destroy",
+           "rasp_shard_allreduce", "rasp_shard_gather")
+
+RASP_GATHER_RESULTS = 1
+RASP_GATHER_OUTPUT = 2
+RASP_GATHER_CONFIG = 4
 
 
 class RaspParams(ctypes.Structure):
@@ -84,6 +91,24 @@ def load():
     lib.rasp_init_c0.restype = ctypes.c_int
     lib.rasp_generate.argtypes = [pp, U64, U64, pb, P]
     lib.rasp_generate.restype = ctypes.c_int
+    lib.rasp_pack.argtypes = [pp, pb, pb, P]
+    lib.rasp_pack.restype = ctypes.c_int
+    lib.rasp_unpack.argtypes = [pp, pb, pb, P]
+    lib.rasp_unpack.restype = ctypes.c_int
+    lib.rasp_topk_workspace_bytes.argtypes = [U32]
+    lib.rasp_topk_workspace_bytes.restype = SZ
+    lib.rasp_topk.argtypes = [P, P, U64, I64, U32, P, P, P, SZ, P]
+    lib.rasp_topk.restype = ctypes.c_int
+    lib.rasp_nccl_unique_id.argtypes = [P]
+    lib.rasp_nccl_unique_id.restype = ctypes.c_int
+    lib.rasp_nccl_comm_init.argtypes = [ctypes.c_int, P, ctypes.c_int, ctypes.POINTER(ctypes.c_void_p)]
+    lib.rasp_nccl_comm_init.restype = ctypes.c_int
+    lib.rasp_nccl_comm_destroy.argtypes = [P]
+    lib.rasp_nccl_comm_destroy.restype = ctypes.c_int
+    lib.rasp_shard_allreduce.argtypes = [P, P, U64, P]
+    lib.rasp_shard_allreduce.restype = ctypes.c_int
+    lib.rasp_shard_gather.argtypes = [P, ctypes.c_int, pp, U64, pb, pb, U32, P]
+    lib.rasp_shard_gather.restype = ctypes.c_int
     lib.rasp_launch_count.argtypes = []
     lib.rasp_launch_count.restype = ctypes.c_ulonglong
     if lib.rasp_abi_version() != ABI_VERSION:
@@ -96,6 +121,6 @@ def check(rc: int, what: str) -> None:
     if rc != 0:
         lib = load()
         msg = lib.rasp_error_string(rc).decode()
-        if rc == -3:
+        if rc in (-3, -6):
             msg += f" ({lib.rasp_last_cuda_error().decode()})"
         raise NativeError(f"{what} failed: {msg} [code {rc}]")

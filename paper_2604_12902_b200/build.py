@@ -63,7 +63,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if proc.wait() != 0:
             raise subprocess.CalledProcessError(proc.returncode, cmd)
         objs.append(obj)
-    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", OUT + ".tmp", *objs]
+    link = [nvcc, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", OUT + ".tmp", *objs, "-ldl"]
     subprocess.run(link, check=True)
     os.replace(OUT + ".tmp", OUT)
     return OUT

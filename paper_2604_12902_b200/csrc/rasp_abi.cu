@@ -27,6 +27,7 @@ const char *rasp_error_string(int code)
     case RASP_ECUDA: return "CUDA error";
     case RASP_EWORKSPACE: return "workspace too small";
     case RASP_EDTYPE: return "word_bytes must be 1, 2, 4 or 8 and hold w bits";
+    case RASP_ENCCL: return "NCCL unavailable or an NCCL call failed";
     default: return "unknown error";
     }
 }

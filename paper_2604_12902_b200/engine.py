@@ -205,3 +205,33 @@ class Engine:
                                         self._stream_ptr(stream))
         _native.check(rc, "rasp_validate")
         return o.cpu().numpy()
+
+    def convert(self, src: DeviceBatch, dst: DeviceBatch, stream=None) -> DeviceBatch:
+        """Word-width conversion src -> dst (rasp_pack / rasp_unpack): e.g. the
+        reference's uint64 arrays into natural-width words, or back."""
+        if src.d != dst.d:
+            raise ValueError("src and dst batches must hold the same number of machines")
+        a, b = src.c_struct(), dst.c_struct()
+        fn = self.lib.rasp_pack if dst.word_bytes <= src.word_bytes else self.lib.rasp_unpack
+        with torch.cuda.device(self.device):
+            rc = fn(ctypes.byref(self._p), ctypes.byref(a), ctypes.byref(b), self._stream_ptr(stream))
+        _native.check(rc, "rasp_pack" if fn is self.lib.rasp_pack else "rasp_unpack")
+        return dst
+
+    def topk(self, batch: DeviceBatch, k: int, tau_max: int, stream=None):
+        """(index, tau_h) int64[k] device tensors of the k longest halting runs,
+        ties to the lower index, -1 padded (rasp_topk)."""
+        if k < 0:
+            raise ValueError(f"k must be >= 0, got {k}")
+        idx = torch.empty(k, dtype=torch.int64, device=self.device)
+        tau = torch.empty(k, dtype=torch.int64, device=self.device)
+        if k == 0:
+            return idx, tau
+        need = self.lib.rasp_topk_workspace_bytes(k)
+        ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        with torch.cuda.device(self.device):
+            rc = self.lib.rasp_topk(batch.status.data_ptr(), batch.tau_h.data_ptr(), batch.d, int(tau_max),
+                                    int(k), idx.data_ptr(), tau.data_ptr(), ws.data_ptr(), need,
+                                    self._stream_ptr(stream))
+        _native.check(rc, "rasp_topk")
+        return idx, tau

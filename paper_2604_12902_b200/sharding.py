@@ -134,3 +134,71 @@ def run_shard_on_device(arrays: dict, params: MachineParams, tau_max: int, epoch
     eng.run(b, tau_max, epoch, fresh=not any(k in arrays for k in ("status", "steps", "tau_h")))
     hist = eng.histogram(b)
     return collect(b.status, b.steps, b.tau_h, b.y, hist, d_total or b.d, gather, group)
+
+
+class NativeComm:
+    """An NCCL communicator owned by the engine library (rasp_nccl_comm_init)
+    for the post-run collectives of a sharded run through the C ABI:
+    rasp_shard_allreduce (histogram + totals) and rasp_shard_gather (per-machine
+    results to the root).  The 128-byte NCCL id travels over the process
+    group that already exists (gloo or nccl), or stays local at world 1."""
+
+    def __init__(self, group=None, device=None):
+        import ctypes
+        from . import _native
+        self.lib = _native.load()
+        self._native = _native
+        initialized = dist.is_available() and dist.is_initialized()
+        self.world = dist.get_world_size(group) if initialized else 1
+        self.rank = dist.get_rank(group) if initialized else 0
+        self.device = torch.device(device) if device is not None else \
+            torch.device("cuda", torch.cuda.current_device())
+        uid = ctypes.create_string_buffer(128)
+        if self.rank == 0:
+            _native.check(self.lib.rasp_nccl_unique_id(uid), "rasp_nccl_unique_id")
+        if self.world > 1:
+            box = [bytes(uid.raw)]
+            dist.broadcast_object_list(box, src=0, group=group)
+            uid = ctypes.create_string_buffer(box[0], 128)
+        self._comm = ctypes.c_void_p()
+        with torch.cuda.device(self.device):
+            _native.check(self.lib.rasp_nccl_comm_init(self.world, uid, self.rank, ctypes.byref(self._comm)),
+                          "rasp_nccl_comm_init")
+
+    def _stream(self, stream):
+        return (stream if stream is not None else torch.cuda.current_stream(self.device)).cuda_stream
+
+    def allreduce(self, counters: torch.Tensor, stream=None) -> torch.Tensor:
+        """In-place sum over ranks of an int64 device tensor."""
+        if counters.dtype != torch.int64 or not counters.is_contiguous():
+            raise ValueError("counters must be a contiguous int64 tensor")
+        with torch.cuda.device(self.device):
+            rc = self.lib.rasp_shard_allreduce(self._comm, counters.data_ptr(), counters.numel(),
+                                               self._stream(stream))
+        self._native.check(rc, "rasp_shard_allreduce")
+        return counters
+
+    def gather(self, shard, full, d_total: int, fields: int, root: int = 0, stream=None):
+        """Gather shard fields (DeviceBatch) into `full` (DeviceBatch of d_total
+        machines, needed on the root only)."""
+        import ctypes
+        p = self._native.RaspParams(shard.params.w, shard.params.n, shard.params.ell, shard.params.s)
+        a = shard.c_struct()
+        b = full.c_struct() if full is not None else None
+        with torch.cuda.device(self.device):
+            rc = self.lib.rasp_shard_gather(self._comm, root, ctypes.byref(p), d_total, ctypes.byref(a),
+                                            ctypes.byref(b) if b is not None else None, fields,
+                                            self._stream(stream))
+        self._native.check(rc, "rasp_shard_gather")
+        return full
+
+    def close(self):
+        if self._comm:
+            self.lib.rasp_nccl_comm_destroy(self._comm)
+            self._comm = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
