@@ -209,6 +209,174 @@ __device__ __forceinline__ void copy_cells(S *__restrict__ dst, const S *__restr
     for (uint64_t k = 0; k < n; ++k) dst[k] = src[k];
 }
 
+
+// --- warp-wide row movement with stmatrix/ldmatrix (shared-memory tiles) --------
+//
+// One `stmatrix.x4` writes 16 bytes of every lane's row (8 u16 or 4 u32
+// cells) into the 32 lane columns, replacing 8 (4) scalar shared stores per
+// lane; `ldmatrix.x4` is the inverse for the write-back.
+//   u32 cells: plain m8n8 -- matrix r row rho is tile row (k0 + r), lanes
+//     4rho..4rho+3, so lane L keeps its natural column L.
+//   u16 cells: the .trans form -- matrix r row rho is tile row
+//     (k0 + 2r + (rho & 1)) holding lanes b, b+4, ..., b+28 (b = rho >> 1), so
+//     lane L's column is position (L & 3) * 8 + (L >> 2) (mx_col).
+// Every lane of the warp must execute these (.sync.aligned).
+template <class SC>
+constexpr bool kMx = sizeof(SC) == 2 || sizeof(SC) == 4;
+
+template <class SC>
+__device__ __forceinline__ uint32_t mx_col(uint32_t lane)
+{
+    if constexpr (sizeof(SC) == 2) return ((lane & 3u) << 3) | (lane >> 2);
+    else return lane;
+}
+
+template <class SC>
+__device__ __forceinline__ uint32_t mx_addr(uint32_t tile0, uint32_t row0, uint32_t lane)
+{
+    if constexpr (sizeof(SC) == 2)
+        return tile0 + (row0 + 2u * (lane >> 3) + (lane & 1u)) * 64u + ((lane >> 1) & 3u) * 16u;
+    else
+        return tile0 + (row0 + (lane >> 3)) * 128u + (lane & 7u) * 16u;
+}
+
+template <class SC>
+__device__ __forceinline__ void stsm(uint32_t addr, const uint4 v)
+{
+    if constexpr (sizeof(SC) == 2)
+        asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};"
+                     ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+    else
+        asm volatile("stmatrix.sync.aligned.m8n8.x4.shared.b16 [%0], {%1, %2, %3, %4};"
+                     ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+
+template <class SC>
+__device__ __forceinline__ uint4 ldsm(uint32_t addr)
+{
+    uint4 v;
+    if constexpr (sizeof(SC) == 2)
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+    else
+        asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+    return v;
+}
+
+// Bytes of HBM row one matrix op covers, and whether rows of `ncells` words
+// starting at `base` can be moved with vector loads of that size.
+template <class S, class SC>
+constexpr uint32_t kMxBytes = (16 / sizeof(SC)) * sizeof(S);
+
+template <class S, class SC>
+__device__ __forceinline__ bool mx_vec_ok(const void *base, uint64_t ncells)
+{
+    constexpr uint32_t GB = kMxBytes<S, SC>;
+    if constexpr (!(sizeof(S) == sizeof(SC) || (sizeof(S) == 1 && sizeof(SC) == 2))) return false;
+    return (reinterpret_cast<uintptr_t>(base) % GB) == 0 && (ncells * sizeof(S)) % GB == 0;
+}
+
+// One lane's 16 bytes of cells [k, k + 16/sizeof(SC)) as SC words.
+template <class S, class SC>
+__device__ __forceinline__ uint4 mx_gather(const S *__restrict__ row, uint32_t k, bool vec)
+{
+    constexpr uint32_t C = 16 / sizeof(SC);
+    if constexpr (sizeof(S) == sizeof(SC)) {
+        if (vec) return *reinterpret_cast<const uint4 *>(row + k);
+    } else if constexpr (sizeof(S) == 1 && sizeof(SC) == 2) {
+        if (vec) {
+            const uint2 w = *reinterpret_cast<const uint2 *>(row + k);
+            return make_uint4(__byte_perm(w.x, 0, 0x4140), __byte_perm(w.x, 0, 0x4342),
+                              __byte_perm(w.y, 0, 0x4140), __byte_perm(w.y, 0, 0x4342));
+        }
+    }
+    uint32_t r[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if constexpr (C == 8)
+            r[q] = (static_cast<uint32_t>(row[k + 2 * q]) & 0xffffu) | (static_cast<uint32_t>(row[k + 2 * q + 1]) << 16);
+        else
+            r[q] = static_cast<uint32_t>(row[k + q]);
+    }
+    return make_uint4(r[0], r[1], r[2], r[3]);
+}
+
+template <class S, class SC>
+__device__ __forceinline__ void mx_scatter(S *__restrict__ row, uint32_t k, const uint4 v, bool vec)
+{
+    constexpr uint32_t C = 16 / sizeof(SC);
+    if constexpr (sizeof(S) == sizeof(SC)) {
+        if (vec) {
+            *reinterpret_cast<uint4 *>(row + k) = v;
+            return;
+        }
+    } else if constexpr (sizeof(S) == 1 && sizeof(SC) == 2) {
+        if (vec) {
+            *reinterpret_cast<uint2 *>(row + k) = make_uint2(__byte_perm(v.x, v.y, 0x6420), __byte_perm(v.z, v.w, 0x6420));
+            return;
+        }
+    }
+    const uint32_t r[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if constexpr (C == 8) {
+            row[k + 2 * q] = static_cast<S>(r[q] & 0xffffu);
+            row[k + 2 * q + 1] = static_cast<S>(r[q] >> 16);
+        } else {
+            row[k + q] = static_cast<S>(r[q]);
+        }
+    }
+}
+
+// Warp-wide: cells [0, ncells) of each valid lane's HBM row -> tile rows
+// row0.. of its column (`col` = the lane's column at row0, for the tail).
+template <class S, class SC, uint32_t B>
+__device__ __forceinline__ void mx_load(const S *__restrict__ row, bool valid, bool vec, uint32_t ncells,
+                                        uint32_t tile0, uint32_t row0, uint32_t lane, SC *col)
+{
+    constexpr uint32_t C = 16 / sizeof(SC);
+    const uint32_t full = ncells / C * C;
+    uint32_t k = 0;
+    for (; k + B * C <= full; k += B * C) {
+        uint4 v[B];
+#pragma unroll
+        for (uint32_t j = 0; j < B; ++j) v[j] = valid ? mx_gather<S, SC>(row, k + j * C, vec) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+        for (uint32_t j = 0; j < B; ++j) stsm<SC>(mx_addr<SC>(tile0, row0 + k + j * C, lane), v[j]);
+    }
+    for (; k < full; k += C) {
+        const uint4 v = valid ? mx_gather<S, SC>(row, k, vec) : make_uint4(0, 0, 0, 0);
+        stsm<SC>(mx_addr<SC>(tile0, row0 + k, lane), v);
+    }
+    if (valid)
+        for (; k < ncells; ++k) col[k * 32] = static_cast<SC>(row[k]);
+}
+
+template <class S, class SC, uint32_t B>
+__device__ __forceinline__ void mx_store(S *__restrict__ row, bool valid, bool vec, uint32_t ncells,
+                                         uint32_t tile0, uint32_t row0, uint32_t lane, const SC *col)
+{
+    constexpr uint32_t C = 16 / sizeof(SC);
+    const uint32_t full = ncells / C * C;
+    uint32_t k = 0;
+    for (; k + B * C <= full; k += B * C) {
+        uint4 v[B];
+#pragma unroll
+        for (uint32_t j = 0; j < B; ++j) v[j] = ldsm<SC>(mx_addr<SC>(tile0, row0 + k + j * C, lane));
+        if (valid) {
+#pragma unroll
+            for (uint32_t j = 0; j < B; ++j) mx_scatter<S, SC>(row, k + j * C, v[j], vec);
+        }
+    }
+    for (; k < full; k += C) {
+        const uint4 v = ldsm<SC>(mx_addr<SC>(tile0, row0 + k, lane));
+        if (valid) mx_scatter<S, SC>(row, k, v, vec);
+    }
+    if (valid)
+        for (; k < ncells; ++k) row[k] = static_cast<S>(col[k * 32]);
+}
+
 // --- one machine per lane -------------------------------------------------------
 //
 // Tile layout per warp: row r holds cell r of all 32 lanes (SC each).
@@ -456,7 +624,9 @@ template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SM
 __global__ void __launch_bounds__(BIG ? 32 : 128, BIG ? 8 : (SMEM ? 10 : 1))
 epoch_kernel(const EpochArgs A, SC *gtiles)
 {
-    constexpr uint32_t LB = BIG ? 32 : 8;   // row-load batch
+    constexpr uint32_t LB = BIG ? 32 : 8;   // row-load batch (per-lane path)
+    // matrix-op batch (16 B per lane each): wide only for native-width rows
+    constexpr uint32_t MB = BIG ? (sizeof(S) == sizeof(SC) ? 32 : 16) : 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr uint32_t ROW = 32 * sizeof(SC);
     const uint32_t lane = threadIdx.x & 31;
@@ -469,7 +639,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     if constexpr (SMEM) {
         tb = reinterpret_cast<char *>(smem_raw);
         lm = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes +
-             lane * static_cast<uint32_t>(sizeof(SC));
+             (kMx<SC> ? mx_col<SC>(lane) : lane) * static_cast<uint32_t>(sizeof(SC));
     } else {
         tb = reinterpret_cast<char *>(gtiles) +
              (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * static_cast<size_t>(tile_bytes);
@@ -484,6 +654,9 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     // lane's HBM output row
     const uint32_t Y = BIG ? 0u : (n + A.g.ell + 1) * ROW + lm;
     constexpr uint32_t YSTEP = BIG ? static_cast<uint32_t>(sizeof(S)) : ROW;
+    constexpr bool MX = SMEM && kMx<SC>;   // warp-wide row moves (stmatrix/ldmatrix)
+    const uint32_t tile0 = SMEM ? static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes : 0u;
+    const bool vecM = mx_vec_ok<S, SC>(A.first ? A.in.M : A.out.M, n) && mx_vec_ok<S, SC>(A.out.M, n);
     char *ybase = nullptr;
     // generic base for the (cold) row copies: gb + address = generic pointer
     char *gb = SMEM ? reinterpret_cast<char *>(smem_raw) -
@@ -541,8 +714,14 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 L.ua = U + static_cast<uint32_t>(srcU[0]) * ROW;
                 L.ya = Y + static_cast<uint32_t>(srcY[0]) * YSTEP;
                 if constexpr (BIG) ybase = reinterpret_cast<char *>(static_cast<S *>(A.out.y) + id * ycols + 1);
-                load_row<S, SC, LB>(srcM, n, reinterpret_cast<SC *>(gb + lm));
-                load_row<S, SC, LB>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
+                if constexpr (!MX) {
+                    load_row<S, SC, LB>(srcM, n, reinterpret_cast<SC *>(gb + lm));
+                    load_row<S, SC, LB>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
+                }
+            }
+            if constexpr (MX) {
+                mx_load<S, SC, MB>(srcM, running, vecM, n, tile0, 0, lane, reinterpret_cast<SC *>(gb + lm));
+                mx_load<S, SC, MB>(srcU + 1, running, false, A.g.ell, tile0, n, lane, reinterpret_cast<SC *>(gb + U));
             }
             const uint64_t rem64 = (steps0 >= A.tau_max) ? 0ull
                                                          : static_cast<uint64_t>(A.tau_max - steps0);
@@ -631,7 +810,14 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 sid = static_cast<uint32_t>(id);
                 if (!fresh) dst.steps[id] = steps0 + K;
             }
-            store_row<S, SC>(static_cast<S *>(dst.M) + id * n, n, reinterpret_cast<const SC *>(gb + lm));
+            if constexpr (!MX)
+                store_row<S, SC>(static_cast<S *>(dst.M) + id * n, n, reinterpret_cast<const SC *>(gb + lm));
+        }
+        if constexpr (MX) {
+            const uint32_t j = tix * 32 + lane;
+            const uint64_t id = running ? (A.list_in ? A.list_in[j] : j) : 0;
+            mx_store<S, SC, MB>(static_cast<S *>(A.out.M) + id * n, running, vecM, n, tile0, 0, lane,
+                                reinterpret_cast<const SC *>(gb + lm));
         }
         const unsigned sv = __ballot_sync(kFull, survivor);
         if (sv) {
