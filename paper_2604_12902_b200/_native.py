@@ -14,7 +14,8 @@ import os
 from .errors import NativeError
 
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
-LIB_PATH = os.path.join(LIB_DIR, "libraspvisor_b200.so")
+# RASP_LIBRARY: load another build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("RASP_LIBRARY") or os.path.join(LIB_DIR, "libraspvisor_b200.so")
 ABI_VERSION = 2
 
 RASP_FRESH = 1

@@ -564,18 +564,73 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
     }
 }
 
-// BIG: tiles of more than 16 KB (few warps per SM): one-warp blocks with a
-// large register budget, so a row load keeps 32 x 16 B in flight.
 // Ungated step, for loop steps of runs whose machines share one budget
 // (every lane has rem >= K, so no lane can run out of budget inside the
 // loop).  A lane is then either live and not fixed -- the step applies -- or
 // sits at a fixed point, where applying the step changes nothing (that is
-// what fixed means: Φ(c) = c, hv:115).  So the update is applied to every
+// what fixed means: Phi(c) = c, hv:115).  So the update is applied to every
 // lane without an "applies" predicate: it only has to honour the cases that
 // leave i in place (opcode outside 1..7, RD at capacity) and never store in
-// them.  This takes the live/fixed bookkeeping off the update chain.
+// them.
+// Fixedness comes for free from the update: for w >= 2 a step that is not a
+// fixed point always moves i ((i+2) mod 2^w != i; a taken BNZ to j != i), and
+// a fixed lane never moves again.  So `moved` is the live flag and L.tlast
+// counts the moves -- the lane's applied steps, i.e. its halting time once it
+// stops moving.  Whether a lane that moved at every step is fixed at the end
+// of the epoch is decided at write-back.
+// YG (big tiles): the output tape is not staged in the tile; PRI stores go
+// straight to the machine's HBM row (ybase + ya, element type YS).
 template <class SC, class CT, bool POW2, Arith AR, bool SMEM, bool YG = false, class YS = SC>
 __device__ __forceinline__ void rasp_step_free(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
+                                               uint32_t yend, const Geo &g, const Opq &q,
+                                               char *ybase = nullptr)
+{
+    static_assert(AR != Arith::W1, "w = 1 uses the gated step");
+    const CT mask = static_cast<CT>(g.mask);
+    const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, base, lm, g, q);
+    const CT a0 = L.a;
+    const bool ucap = L.ua >= uend;
+    const bool taken = (f.o == 5) & ((AR == Arith::CELL ? (a0 & mask) : a0) != 0);
+    const bool stay = (static_cast<CT>(f.o - 1) > 6) | ((f.o == 6) & ucap);   // i does not move
+    if (f.o == 1) L.a = f.jw;
+    if constexpr (AR == Arith::CELL) {
+        if (f.o == 2) L.a = a0 + f.mj;
+        if (f.o == 3) L.a = a0 * f.mj;
+    } else {
+        if (f.o == 2) L.a = wrap<CT, AR>(a0 + f.mj, mask);
+        if (f.o == 3) L.a = wrap<CT, AR>(a0 * f.mj, mask);
+    }
+    if (f.o == 4) st_cell<SC, CT, SMEM>(base, f.jo, a0);
+    if ((f.o == 6) & !ucap) {
+        st_cell<SC, CT, SMEM>(base, f.jo, f.ud);
+        L.ua += q.row;
+    }
+    if constexpr (YG) {   // HBM row: lanes without a machine must not store
+        if (L.active & (f.o == 7) & (L.ya < yend)) {
+            *reinterpret_cast<YS *>(ybase + L.ya) = static_cast<YS>(f.mj);
+            L.ya += static_cast<uint32_t>(sizeof(YS));
+        }
+    } else if ((f.o == 7) & (L.ya < yend)) {
+        st_cell<SC, CT, SMEM>(base, L.ya, f.mj);
+        L.ya += q.row;
+    }
+    CT i2;
+    if constexpr (kRawI<POW2, AR>) i2 = L.i + static_cast<CT>(q.two);
+    else i2 = wrap<CT, AR>(L.i + 2, mask);
+    const CT ni = taken ? f.jw : (stay ? L.i : i2);
+    bool moved;
+    if constexpr (kRawI<POW2, AR> && AR != Arith::FULL) moved = ((ni ^ L.i) & mask) != 0;
+    else moved = ni != L.i;
+    L.active = moved;
+    if (moved) ++L.tlast;
+    L.i = ni;
+}
+
+// The explicit form of the ungated step (active &= !fixed; tlast = t while
+// live): the big-tile kernels, latency- rather than issue-bound, run faster
+// with it.
+template <class SC, class CT, bool POW2, Arith AR, bool SMEM, bool YG = false, class YS = SC>
+__device__ __forceinline__ void rasp_step_free_t(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
                                                uint32_t yend, const Geo &g, const Opq &q, uint32_t t,
                                                char *ybase = nullptr)
 {
@@ -620,13 +675,14 @@ __device__ __forceinline__ void rasp_step_free(LaneState<CT> &L, char *base, uin
     L.i = taken ? f.jw : (stay ? L.i : i2);
 }
 
+
 template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM, bool BIG = false>
 __global__ void __launch_bounds__(BIG ? 32 : 128, BIG ? 8 : (SMEM ? 10 : 1))
 epoch_kernel(const EpochArgs A, SC *gtiles)
 {
     constexpr uint32_t LB = BIG ? 32 : 8;   // row-load batch (per-lane path)
     // matrix-op batch (16 B per lane each): wide only for native-width rows
-    constexpr uint32_t MB = BIG ? (sizeof(S) == sizeof(SC) ? 32 : 16) : 4;
+    constexpr uint32_t MB = 4;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr uint32_t ROW = 32 * sizeof(SC);
     const uint32_t lane = threadIdx.x & 31;
@@ -639,7 +695,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     if constexpr (SMEM) {
         tb = reinterpret_cast<char *>(smem_raw);
         lm = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes +
-             (kMx<SC> ? mx_col<SC>(lane) : lane) * static_cast<uint32_t>(sizeof(SC));
+             ((kMx<SC> && !BIG) ? mx_col<SC>(lane) : lane) * static_cast<uint32_t>(sizeof(SC));
     } else {
         tb = reinterpret_cast<char *>(gtiles) +
              (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + wib) * static_cast<size_t>(tile_bytes);
@@ -654,7 +710,12 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     // lane's HBM output row
     const uint32_t Y = BIG ? 0u : (n + A.g.ell + 1) * ROW + lm;
     constexpr uint32_t YSTEP = BIG ? static_cast<uint32_t>(sizeof(S)) : ROW;
-    constexpr bool MX = SMEM && kMx<SC>;   // warp-wide row moves (stmatrix/ldmatrix)
+    // warp-wide row moves (stmatrix/ldmatrix); BIG tiles keep per-lane moves
+    // with 32 loads in flight (measured faster for their few resident warps)
+    constexpr bool MX = SMEM && kMx<SC> && !BIG;
+    // ungated steps with move counting (every lane's budget covers the epoch;
+    // issue-bound shared-memory tiles -- big tiles keep the explicit form)
+    constexpr bool kCount = !BUDGET && AR != Arith::W1 && !BIG;
     const uint32_t tile0 = SMEM ? static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes : 0u;
     const bool vecM = mx_vec_ok<S, SC>(A.first ? A.in.M : A.out.M, n) && mx_vec_ok<S, SC>(A.out.M, n);
     char *ybase = nullptr;
@@ -718,6 +779,11 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                     load_row<S, SC, LB>(srcM, n, reinterpret_cast<SC *>(gb + lm));
                     load_row<S, SC, LB>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
                 }
+            } else if constexpr (kCount && !MX) {
+                // a lane without a machine sits at a fixed point (opcode 0 at
+                // i = 0), so move-counting steps never see it move (the matrix
+                // loads zero-fill such columns)
+                reinterpret_cast<SC *>(gb + lm)[0] = 0;
             }
             if constexpr (MX) {
                 mx_load<S, SC, MB>(srcM, running, vecM, n, tile0, 0, lane, reinterpret_cast<SC *>(gb + lm));
@@ -736,30 +802,43 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const uint32_t yend = Y + g.s * YSTEP;
             uint32_t t = 0;
             bool live = __any_sync(kFull, L.active);
-            if constexpr (!BUDGET && AR != Arith::W1) {
+            if constexpr (kCount) {
                 for (; live && t + 2 <= K; t += 2) {
-                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, ybase);
-                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, ybase);
+                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, ybase);
+                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, ybase);
                     live = __any_sync(kFull, L.active);
                 }
                 if (live && t < K) {
-                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, ybase);
+                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, ybase);
                     ++t;
                     live = __any_sync(kFull, L.active);
                 }
             } else {
-                for (; live && t + 2 <= K; t += 2) {
-                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
-                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, true, ybase);
-                    live = __any_sync(kFull, L.active);
+                if constexpr (!BUDGET && AR != Arith::W1) {
+                    for (; live && t + 2 <= K; t += 2) {
+                        rasp_step_free_t<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, ybase);
+                        rasp_step_free_t<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, ybase);
+                        live = __any_sync(kFull, L.active);
+                    }
+                    if (live && t < K) {
+                        rasp_step_free_t<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, ybase);
+                        ++t;
+                        live = __any_sync(kFull, L.active);
+                    }
+                } else {
+                    for (; live && t + 2 <= K; t += 2) {
+                        rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
+                        rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, true, ybase);
+                        live = __any_sync(kFull, L.active);
+                    }
+                    if (live && t < K) {
+                        rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
+                        ++t;
+                        live = __any_sync(kFull, L.active);
+                    }
                 }
-                if (live && t < K) {
-                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
-                    ++t;
-                    live = __any_sync(kFull, L.active);
-                }
+                if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
             }
-            if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
         }
         if (lane == 0) next = atomicAdd(&sc->tile_ctr[e], 1u);   // overlaps the write-back
 
@@ -787,15 +866,28 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             static_cast<S *>(dst.iw)[id] = static_cast<S>(L.i);
             static_cast<S *>(dst.ac)[id] = static_cast<S>(L.a);
             static_cast<S *>(dst.u)[id * ucols] = static_cast<S>(u0);
-            if (!L.active) {
+            bool fin, halted = true;
+            if constexpr (kCount) {
+                // tlast = moves: below K the lane stopped moving (fixed there);
+                // at K it is fixed at K, out of budget (K == rem), or survives
+                fin = L.tlast < K;
+                if (!fin) {
+                    const uint32_t uend = U + A.g.ell * ROW, yend = Y + A.g.s * YSTEP;
+                    const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, tb, lm, A.g, q);
+                    halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, A.g, q);
+                    fin = halted | (K == L.rem);
+                }
+            } else {
                 // verdict at tlast: halted, unless the budget ran out there and
                 // the configuration is not a fixed point
-                bool halted = true;
-                if (L.tlast == L.rem) {
+                fin = !L.active;
+                if (fin && L.tlast == L.rem) {
                     const uint32_t uend = U + A.g.ell * ROW, yend = Y + A.g.s * YSTEP;
                     const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, tb, lm, A.g, q);
                     halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, A.g, q);
                 }
+            }
+            if (fin) {
                 const int64_t tend = steps0 + L.tlast;
                 dst.steps[id] = tend;
                 if (!halted) {
