@@ -368,8 +368,6 @@ def main():
     for _ in range(max(args.warmup, 0)):
         one_step()
     torch.cuda.synchronize()
-    machine_steps = int(dst.steps.sum().item())
-    halted = int((dst.status == 1).sum().item())
 
     # --- timed region: device time per step with CUDA events; L2 flushed between steps
     clocks = ClockSampler(local_rank)
@@ -395,6 +393,8 @@ def main():
     wall = time.perf_counter() - t_wall0
     launches = lib.rasp_launch_count() - launches0
     clk = clocks.stop()
+    machine_steps = int(dst.steps.sum().item())   # identical every step (deterministic run)
+    halted = int((dst.status == 1).sum().item())
     per_step = [a.elapsed_time(b) / 1e3 for a, b in evs]
     t_step = statistics.mean(per_step)
     # kernel-only time of rasp_run (dominant kernel: the epoch kernel)

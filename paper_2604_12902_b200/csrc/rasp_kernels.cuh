@@ -377,6 +377,16 @@ __device__ __forceinline__ void mx_store(S *__restrict__ row, bool valid, bool v
         for (; k < ncells; ++k) row[k] = static_cast<S>(col[k * 32]);
 }
 
+
+// Bulk L2 prefetch of [p, p + bytes) (rounded out to 16-byte granules).
+__device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes)
+{
+    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+    const uintptr_t lo = a & ~uintptr_t(15), hi = (a + bytes + 15) & ~uintptr_t(15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(static_cast<uint32_t>(hi - lo))
+                 : "memory");
+}
+
 // --- one machine per lane -------------------------------------------------------
 //
 // Tile layout per warp: row r holds cell r of all 32 lanes (SC each).
@@ -731,6 +741,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     const int64_t covered = A.first ? 0 : sc->covered[e];
     const uint32_t ntiles = (K == 0 && !A.first) ? 0 : (count + 31) / 32;
     if (ntiles == 0) return;   // schedule finished: K[e+1] stays 0 from the memset
+    const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
     const bool copy_side = A.first && !A.inplace;
     const bool fresh = A.fresh != 0;
 
@@ -795,6 +806,19 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             L.active = running;
         }
         asm volatile("" ::: "memory");   // column fills above are visible to the asm loads below
+        {   // warm L2 with the tile this warp will probably take next (tiles are
+            // claimed in order, about one per resident warp ahead): its rows
+            // then arrive from L2 while the epoch's DRAM traffic streams behind
+            const uint32_t pf = tix + nwarps;
+            const uint32_t j = pf * 32 + lane;
+            if (pf < ntiles && j < count) {
+                const Side &src = A.first ? A.in : A.out;
+                const uint64_t id = A.list_in ? A.list_in[j] : j;
+                prefetch_l2(static_cast<const S *>(src.M) + id * n, n * static_cast<uint32_t>(sizeof(S)));
+                prefetch_l2(static_cast<const S *>(src.u) + id * (static_cast<uint64_t>(A.g.ell) + 1),
+                            (A.g.ell + 1) * static_cast<uint32_t>(sizeof(S)));
+            }
+        }
 
         {   // ---- step loop
             const Geo g = A.g;
