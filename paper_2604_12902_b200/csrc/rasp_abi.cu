@@ -87,6 +87,8 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.row = uint32_t(32 * cell_bytes(p->w));
     a.stable_q8 = 128;                       // 0.5 (measured best on C2 and C5): tuning knob RASP_STABLE_Q8
     if (const char *e = std::getenv("RASP_STABLE_Q8")) a.stable_q8 = uint32_t(std::strtoul(e, nullptr, 10));
+    a.pf_dist = 1;                           // tuning knob RASP_PREFETCH (0 disables)
+    if (const char *e = std::getenv("RASP_PREFETCH")) a.pf_dist = uint32_t(std::strtoul(e, nullptr, 10));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!a.inplace) {
         // out-of-place: the input tapes and the bookkeeping arrays move in bulk;

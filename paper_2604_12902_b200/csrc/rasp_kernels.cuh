@@ -60,6 +60,10 @@ struct Side {
 
 constexpr int kMaxEpochs = 1024;
 
+#ifndef RASP_UNROLL
+#define RASP_UNROLL 8
+#endif
+
 // Device-side epoch schedule (workspace).  Epoch e reads its length K[e] and
 // start offset covered[e]; the last block of epoch e writes K[e+1] from the
 // survival ratio it observed, so the host can enqueue epochs without
@@ -90,6 +94,7 @@ struct EpochArgs {
     uint32_t one, two;             // the constants 1 and 2 (see Opq)
     uint32_t row;                  // bytes per tile row (32 * sizeof(SC))
     uint32_t stable_q8;            // survival ratio (x256) at which the rest runs as one epoch
+    uint32_t pf_dist;              // L2 prefetch distance in rounds of resident warps (0: off)
 };
 
 template <class CT, Arith AR>
@@ -726,6 +731,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     // ungated steps with move counting (every lane's budget covers the epoch;
     // issue-bound shared-memory tiles -- big tiles keep the explicit form)
     constexpr bool kCount = !BUDGET && AR != Arith::W1 && !BIG;
+    constexpr uint32_t kUnroll = RASP_UNROLL;
     const uint32_t tile0 = SMEM ? static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes : 0u;
     const bool vecM = mx_vec_ok<S, SC>(A.first ? A.in.M : A.out.M, n) && mx_vec_ok<S, SC>(A.out.M, n);
     char *ybase = nullptr;
@@ -809,9 +815,9 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
         {   // warm L2 with the tile this warp will probably take next (tiles are
             // claimed in order, about one per resident warp ahead): its rows
             // then arrive from L2 while the epoch's DRAM traffic streams behind
-            const uint32_t pf = tix + nwarps;
+            const uint32_t pf = tix + A.pf_dist * nwarps;
             const uint32_t j = pf * 32 + lane;
-            if (pf < ntiles && j < count) {
+            if (A.pf_dist && pf < ntiles && j < count) {
                 const Side &src = A.first ? A.in : A.out;
                 const uint64_t id = A.list_in ? A.list_in[j] : j;
                 prefetch_l2(static_cast<const S *>(src.M) + id * n, n * static_cast<uint32_t>(sizeof(S)));
@@ -826,27 +832,30 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const uint32_t yend = Y + g.s * YSTEP;
             uint32_t t = 0;
             bool live = __any_sync(kFull, L.active);
+            // steps between live checks (the check ends each block with a vote
+            // and a branch the next block's loads wait on)
+            constexpr uint32_t UN = kUnroll;
             if constexpr (kCount) {
-                for (; live && t + 2 <= K; t += 2) {
-                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, ybase);
-                    rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, ybase);
+                for (; live && t + UN <= K; t += UN) {
+#pragma unroll
+                    for (uint32_t r = 0; r < UN; ++r)
+                        rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, ybase);
                     live = __any_sync(kFull, L.active);
                 }
-                if (live && t < K) {
+                for (; live && t < K; ++t) {
                     rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, ybase);
-                    ++t;
                     live = __any_sync(kFull, L.active);
                 }
             } else {
                 if constexpr (!BUDGET && AR != Arith::W1) {
-                    for (; live && t + 2 <= K; t += 2) {
-                        rasp_step_free_t<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, ybase);
-                        rasp_step_free_t<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, ybase);
+                    for (; live && t + UN <= K; t += UN) {
+#pragma unroll
+                        for (uint32_t r = 0; r < UN; ++r)
+                            rasp_step_free_t<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + r, ybase);
                         live = __any_sync(kFull, L.active);
                     }
-                    if (live && t < K) {
+                    for (; live && t < K; ++t) {
                         rasp_step_free_t<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, ybase);
-                        ++t;
                         live = __any_sync(kFull, L.active);
                     }
                 } else {
