@@ -278,6 +278,9 @@ def bench_enumeration(args, world, rank, dev, desc):
         dist.destroy_process_group()
 
 
+DEFAULT_EPOCH = {"c1": 64, "c2": 48, "c3": 48, "c5": 256, "paper": 32}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -285,12 +288,18 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--epoch", type=int, default=64)   # BatchConfig.epoch default (hv:170)
+    # first epoch length (the reference's q, BatchConfig.epoch, hv:170): a
+    # performance knob only -- results are independent of it.  Default per
+    # config from sweeps on B200 (scripts/sweep_epoch.sh): heavy machines
+    # (C5: 1.3 KB of tile each) amortise their load over a longer first epoch
+    ap.add_argument("--epoch", type=int, default=None)
     # machines in the CPU baseline's sample: the whole batch up to 2^20 (c2, c5 and
     # paper run in full; c3 runs 2^20 of its 16M; c4 runs 2^18 programs)
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.epoch is None:
+        args.epoch = DEFAULT_EPOCH.get(args.config, 64)
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
