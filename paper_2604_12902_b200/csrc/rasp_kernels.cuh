@@ -691,6 +691,101 @@ __device__ __forceinline__ void rasp_step_free_t(LaneState<CT> &L, char *base, u
 }
 
 
+__device__ __forceinline__ uint32_t sel32(bool c, uint32_t a, uint32_t b)
+{
+    uint32_t r;
+    asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tselp.b32 %0, %1, %2, p;\n\t}"
+        : "=r"(r) : "r"(a), "r"(b), "r"(static_cast<uint32_t>(c)));
+    return r;
+}
+
+// c ? a : b as a select instruction (ptxas otherwise sometimes turns an
+// opcode-keyed chain of conditional updates into a branch tree)
+template <class CT>
+__device__ __forceinline__ CT selw(bool c, CT a, CT b)
+{
+    if constexpr (sizeof(CT) == 8) {
+        unsigned long long r;
+        asm("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %3, 0;\n\tselp.b64 %0, %1, %2, p;\n\t}"
+            : "=l"(r) : "l"(static_cast<unsigned long long>(a)), "l"(static_cast<unsigned long long>(b)),
+              "r"(static_cast<uint32_t>(c)));
+        return static_cast<CT>(r);
+    } else {
+        return static_cast<CT>(sel32(c, static_cast<uint32_t>(a), static_cast<uint32_t>(b)));
+    }
+}
+
+// Ungated step for n not a power of two.  Instead of reducing i and i+1 mod n
+// (a multiply-high chain each) before every fetch, the residues im = i mod n
+// and ib = ((i+1) mod 2^w) mod n are carried from step to step: an advance
+// adds 2 (one conditional subtract of n, and i+2 wrapping through 2^w lands
+// on 0 or 1, its own residue), a taken branch reuses j mod n, which the
+// M[j] access computes anyway.  COUNT selects the move-counting form of
+// rasp_step_free, else the explicit form of rasp_step_free_t.
+template <class SC, class CT, Arith AR, bool SMEM, bool COUNT, bool YG = false, class YS = SC>
+__device__ __forceinline__ void rasp_step_inc(LaneState<CT> &L, uint32_t &im, uint32_t &ib, char *base,
+                                              uint32_t lm, uint32_t uend, uint32_t yend, const Geo &g,
+                                              const Opq &q, uint32_t t, char *ybase = nullptr)
+{
+    static_assert(AR != Arith::W1, "w = 1 uses the gated step");
+    constexpr uint32_t SH = sizeof(SC) == 2 ? 6 : sizeof(SC) == 4 ? 7 : 8;   // log2(row bytes)
+    const CT mask = static_cast<CT>(g.mask);
+    const CT o = ld_cell<SC, CT, SMEM>(base, (im << SH) + lm);
+    const CT jw = ld_cell<SC, CT, SMEM>(base, (ib << SH) + lm);
+    const uint32_t jn = modn<CT, false>(jw, g);
+    const uint32_t jo = (jn << SH) + lm;
+    const CT mj = ld_cell<SC, CT, SMEM>(base, jo);
+    const CT ud = ld_cell<SC, CT, SMEM>(base, L.ua);
+    const CT a0 = L.a;
+    const bool ucap = L.ua >= uend;
+    const bool taken = (o == 5) & ((AR == Arith::CELL ? (a0 & mask) : a0) != 0);
+    const bool stay = (static_cast<CT>(o - 1) > 6) | ((o == 6) & ucap);   // i does not move
+    if constexpr (!COUNT) {
+        const bool fixed = stay | (taken & (jw == L.i));
+        if (L.active) L.tlast = t;
+        L.active = L.active & !fixed;
+    }
+    {
+        CT na = selw<CT>(o == 1, jw, a0);
+        if constexpr (AR == Arith::CELL) {
+            na = selw<CT>(o == 2, a0 + mj, na);
+            na = selw<CT>(o == 3, a0 * mj, na);
+        } else {
+            na = selw<CT>(o == 2, wrap<CT, AR>(a0 + mj, mask), na);
+            na = selw<CT>(o == 3, wrap<CT, AR>(a0 * mj, mask), na);
+        }
+        L.a = na;
+    }
+    if (o == 4) st_cell<SC, CT, SMEM>(base, jo, a0);
+    if ((o == 6) & !ucap) {
+        st_cell<SC, CT, SMEM>(base, jo, ud);
+        L.ua += q.row;
+    }
+    if constexpr (YG) {   // HBM row: lanes without a machine (no ybase) must not store
+        if (L.active & (o == 7) & (L.ya < yend)) {
+            *reinterpret_cast<YS *>(ybase + L.ya) = static_cast<YS>(mj);
+            L.ya += static_cast<uint32_t>(sizeof(YS));
+        }
+    } else if ((o == 7) & (L.ya < yend)) {
+        st_cell<SC, CT, SMEM>(base, L.ya, mj);
+        L.ya += q.row;
+    }
+    const CT i2 = wrap<CT, AR>(L.i + 2, mask);
+    uint32_t im2 = im + 2;
+    im2 = im2 >= g.n ? im2 - g.n : im2;
+    im2 = i2 < 2 ? static_cast<uint32_t>(i2) : im2;      // wrapped through 2^w
+    const CT ni = selw<CT>(taken, jw, selw<CT>(stay, L.i, i2));
+    im = sel32(taken, jn, sel32(stay, im, im2));
+    const uint32_t ib1 = im + 1;
+    ib = sel32((ib1 == g.n) | (ni == mask), 0u, ib1);
+    if constexpr (COUNT) {
+        const bool moved = ni != L.i;
+        L.active = moved;
+        if (moved) ++L.tlast;
+    }
+    L.i = ni;
+}
+
 template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM, bool BIG = false>
 __global__ void __launch_bounds__(BIG ? 32 : 128, BIG ? 8 : (SMEM ? 10 : 1))
 epoch_kernel(const EpochArgs A, SC *gtiles)
@@ -731,6 +826,8 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     // ungated steps with move counting (every lane's budget covers the epoch;
     // issue-bound shared-memory tiles -- big tiles keep the explicit form)
     constexpr bool kCount = !BUDGET && AR != Arith::W1 && !BIG;
+    // ungated steps with carried residues (n not a power of two)
+    constexpr bool kInc = !BUDGET && AR != Arith::W1 && !POW2 && SMEM;
     constexpr uint32_t kUnroll = RASP_UNROLL;
     const uint32_t tile0 = SMEM ? static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes : 0u;
     const bool vecM = mx_vec_ok<S, SC>(A.first ? A.in.M : A.out.M, n) && mx_vec_ok<S, SC>(A.out.M, n);
@@ -835,7 +932,23 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             // steps between live checks (the check ends each block with a vote
             // and a branch the next block's loads wait on)
             constexpr uint32_t UN = kUnroll;
-            if constexpr (kCount) {
+            if constexpr (kInc) {
+                // residues of i and i+1 mod n, carried across steps
+                uint32_t im = modn<CT, false>(L.i, g);
+                uint32_t ib = modn<CT, false>(wrap<CT, AR>(L.i + 1, static_cast<CT>(g.mask)), g);
+                for (; live && t + UN <= K; t += UN) {
+#pragma unroll
+                    for (uint32_t r = 0; r < UN; ++r)
+                        rasp_step_inc<SC, CT, AR, SMEM, kCount, BIG, S>(L, im, ib, tb, lm, uend, yend, g, q, t + r, ybase);
+                    live = __any_sync(kFull, L.active);
+                }
+                for (; live && t < K; ++t) {
+                    rasp_step_inc<SC, CT, AR, SMEM, kCount, BIG, S>(L, im, ib, tb, lm, uend, yend, g, q, t, ybase);
+                    live = __any_sync(kFull, L.active);
+                }
+                if constexpr (!kCount)
+                    if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
+            } else if constexpr (kCount) {
                 for (; live && t + UN <= K; t += UN) {
 #pragma unroll
                     for (uint32_t r = 0; r < UN; ++r)
