@@ -186,7 +186,10 @@ def test_large_batch_against_oracle_sample(pkg):
 
 
 @pytest.mark.parametrize("shape", [(8, 8, 2, 2), (16, 16, 2, 2), (16, 64, 8, 8), (32, 250, 10, 2),
-                                   (32, 64, 4, 2), (64, 12, 3, 3), (5, 7, 3, 2), (1, 6, 1, 1)])
+                                   (32, 64, 4, 2), (64, 12, 3, 3), (5, 7, 3, 2), (1, 6, 1, 1),
+                                   # n not a power of two on every tile kind (carried residues)
+                                   (8, 250, 10, 2), (12, 100, 4, 4), (16, 100, 8, 8), (32, 100, 4, 2),
+                                   (24, 30, 3, 3), (3, 6, 2, 2), (64, 250, 4, 2)])
 def test_random_midrun_configs_against_oracle(pkg, shape):
     """Arbitrary mid-run configurations (every step case, odd i, full tapes,
     wrapped addresses) at 8K machines per shape, several epochs."""
