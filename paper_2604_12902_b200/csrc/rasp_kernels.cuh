@@ -986,33 +986,10 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
             }
         }
-        if (lane == 0) next = atomicAdd(&sc->tile_ctr[e], 1u);   // overlaps the write-back
-
-        bool survivor = false;
-        uint32_t sid = 0;
-        if (running) {   // ---- write-back phase (re-derives what the load phase knew)
-            const Side &src = A.first ? A.in : A.out;
-            const Side &dst = A.out;
-            const uint64_t ucols = static_cast<uint64_t>(A.g.ell) + 1;
-            const uint64_t ycols = static_cast<uint64_t>(A.g.s) + 1;
-            const uint32_t j = tix * 32 + lane;
-            const uint64_t id = A.list_in ? A.list_in[j] : j;
-            const int64_t steps0 = fresh ? covered : dst.steps[id];
-            const uint32_t y0_start = static_cast<uint32_t>(static_cast<const S *>(src.y)[id * ycols]);
-            const uint32_t u0 = (L.ua - U) / ROW;
-            const uint32_t y0 = (L.ya - Y) / YSTEP;
-            if constexpr (kRawI<POW2, AR>) L.i &= static_cast<CT>(A.g.mask);
-            if constexpr (AR == Arith::CELL) L.a &= static_cast<CT>(A.g.mask);
-            S *dY = static_cast<S *>(dst.y) + id * ycols;
-            if constexpr (!BIG) {
-                const SC *colY = reinterpret_cast<const SC *>(gb + Y);
-                for (uint32_t k = y0_start; k < y0; ++k) dY[k + 1] = static_cast<S>(colY[k * 32]);
-            }
-            dY[0] = static_cast<S>(y0);
-            static_cast<S *>(dst.iw)[id] = static_cast<S>(L.i);
-            static_cast<S *>(dst.ac)[id] = static_cast<S>(L.a);
-            static_cast<S *>(dst.u)[id * ucols] = static_cast<S>(u0);
-            bool fin, halted = true;
+        // ---- verdicts first, so the two atomics (next tile, survivor slots)
+        // are in flight while the write-back stores issue
+        bool fin = false, halted = true;
+        if (running) {
             if constexpr (kCount) {
                 // tlast = moves: below K the lane stopped moving (fixed there);
                 // at K it is fixed at K, out of budget (K == rem), or survives
@@ -1033,6 +1010,38 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                     halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, A.g, q);
                 }
             }
+        }
+        const bool survivor = running & !fin;
+        const unsigned sv = __ballot_sync(kFull, survivor);
+        uint32_t sbase = 0;
+        if (lane == 0) {
+            next = atomicAdd(&sc->tile_ctr[e], 1u);
+            if (sv) sbase = atomicAdd(&sc->count[e], static_cast<uint32_t>(__popc(sv)));
+        }
+
+        uint64_t id = 0;
+        if (running) {   // ---- write-back phase (re-derives what the load phase knew)
+            const Side &src = A.first ? A.in : A.out;
+            const Side &dst = A.out;
+            const uint64_t ucols = static_cast<uint64_t>(A.g.ell) + 1;
+            const uint64_t ycols = static_cast<uint64_t>(A.g.s) + 1;
+            const uint32_t j = tix * 32 + lane;
+            id = A.list_in ? A.list_in[j] : j;
+            const int64_t steps0 = fresh ? covered : dst.steps[id];
+            const uint32_t y0_start = static_cast<uint32_t>(static_cast<const S *>(src.y)[id * ycols]);
+            const uint32_t u0 = (L.ua - U) / ROW;
+            const uint32_t y0 = (L.ya - Y) / YSTEP;
+            if constexpr (kRawI<POW2, AR>) L.i &= static_cast<CT>(A.g.mask);
+            if constexpr (AR == Arith::CELL) L.a &= static_cast<CT>(A.g.mask);
+            S *dY = static_cast<S *>(dst.y) + id * ycols;
+            if constexpr (!BIG) {
+                const SC *colY = reinterpret_cast<const SC *>(gb + Y);
+                for (uint32_t k = y0_start; k < y0; ++k) dY[k + 1] = static_cast<S>(colY[k * 32]);
+            }
+            dY[0] = static_cast<S>(y0);
+            static_cast<S *>(dst.iw)[id] = static_cast<S>(L.i);
+            static_cast<S *>(dst.ac)[id] = static_cast<S>(L.a);
+            static_cast<S *>(dst.u)[id * ucols] = static_cast<S>(u0);
             if (fin) {
                 const int64_t tend = steps0 + L.tlast;
                 dst.steps[id] = tend;
@@ -1043,26 +1052,18 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                     dst.status[id] = kHalted;
                     dst.tau_h[id] = tend;
                 }
-            } else {
-                survivor = true;
-                sid = static_cast<uint32_t>(id);
-                if (!fresh) dst.steps[id] = steps0 + K;
+            } else if (!fresh) {
+                dst.steps[id] = steps0 + K;
             }
             if constexpr (!MX)
                 store_row<S, SC>(static_cast<S *>(dst.M) + id * n, n, reinterpret_cast<const SC *>(gb + lm));
         }
-        if constexpr (MX) {
-            const uint32_t j = tix * 32 + lane;
-            const uint64_t id = running ? (A.list_in ? A.list_in[j] : j) : 0;
+        if constexpr (MX)
             mx_store<S, SC, MB>(static_cast<S *>(A.out.M) + id * n, running, vecM, n, tile0, 0, lane,
                                 reinterpret_cast<const SC *>(gb + lm));
-        }
-        const unsigned sv = __ballot_sync(kFull, survivor);
         if (sv) {
-            uint32_t base = 0;
-            if (lane == 0) base = atomicAdd(&sc->count[e], static_cast<uint32_t>(__popc(sv)));
-            base = __shfl_sync(kFull, base, 0);
-            if (survivor) A.list_out[base + __popc(sv & ((1u << lane) - 1u))] = sid;
+            sbase = __shfl_sync(kFull, sbase, 0);
+            if (survivor) A.list_out[sbase + __popc(sv & ((1u << lane) - 1u))] = static_cast<uint32_t>(id);
         }
     }
 
