@@ -151,7 +151,8 @@ int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t cou
     int per_sm = 0;
     RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
     if (per_sm < 1) return RASP_ECAPACITY;
-    const uint64_t grid = std::min<uint64_t>(count, uint64_t(per_sm) * dv.nsm * 8);
+    // one resident wave of blocks; every warp loops over whole programs
+    const uint64_t grid = std::min<uint64_t>((count + 7) / 8, uint64_t(per_sm) * dv.nsm);
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     kern<<<unsigned(grid), 256, smem, st>>>(a);
     RASP_CUDA(cudaGetLastError());

@@ -1129,11 +1129,12 @@ template <bool POW2, Arith AR>
 __global__ void __launch_bounds__(256)
 enum_kernel(const EnumArgs A)
 {
+    // Each warp takes whole programs: the 2^w inputs of a program run as
+    // groups of 32 lanes on the warp's tile, one after the other, and the warp
+    // alone reduces them into the program's record (no block barriers).
     using SC = uint16_t;
     using CT = uint32_t;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    __shared__ unsigned long long red_sum[8];
-    __shared__ unsigned int red_all[8];
     __shared__ unsigned long long red_steps[8];
     constexpr uint32_t ROW = 32 * sizeof(SC);
     const uint32_t lane = threadIdx.x & 31;
@@ -1142,91 +1143,87 @@ enum_kernel(const EnumArgs A)
     const uint32_t n = g.n;
     const uint32_t tile_bytes = (n + 3) * ROW;     // M, u[1] + pad, y[1]
     char *tb = reinterpret_cast<char *>(smem_raw);
-    const uint32_t lm = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes +
-                        lane * static_cast<uint32_t>(sizeof(SC));
+    const uint32_t tile0 = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes;
+    const uint32_t lm = tile0 + lane * static_cast<uint32_t>(sizeof(SC));
     char *gb = reinterpret_cast<char *>(smem_raw) - static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
-    SC *colM = reinterpret_cast<SC *>(gb + lm);
     const uint32_t U = n * ROW + lm, Y = (n + 2) * ROW + lm;
     const uint32_t uend = U + ROW, yend = Y + ROW;
     const Opq q = {1u, 2u, ROW};
     const uint32_t pw = A.ob + A.pb;
-    const uint32_t x = threadIdx.x;                 // the input word of this lane
-    const bool valid_x = x <= static_cast<uint32_t>(g.mask);
+    const uint32_t xs = static_cast<uint32_t>(g.mask) + 1;   // inputs per program (2^w)
+    const uint32_t groups = (xs + 31) / 32;
+    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    unsigned long long my_steps = 0;
 
-    for (uint64_t pi = blockIdx.x; pi < A.count; pi += gridDim.x) {
+    for (uint64_t pi = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + wib; pi < A.count; pi += nwarps) {
         const uint64_t r = A.first + pi;
-        // c0: decode the program into M, input x into u[1], empty output
-        for (uint32_t k = 0; k < n; ++k) colM[k * 32] = 0;
-        for (uint32_t k = 0; k < A.m && 2 * k + 1 < n; ++k) {
-            const uint32_t pair = static_cast<uint32_t>(r >> (k * pw)) & ((1u << pw) - 1u);
-            colM[(2 * k) * 32] = static_cast<SC>(pair & ((1u << A.ob) - 1u));
-            colM[(2 * k + 1) * 32] = static_cast<SC>(pair >> A.ob);
-        }
-        *reinterpret_cast<SC *>(gb + U) = static_cast<SC>(x);
-        LaneState<CT> L;
-        L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tlast = 0; L.rem = A.tau;
-        L.active = valid_x;
-        asm volatile("" ::: "memory");
-        const uint32_t K = A.tau;
-        uint32_t t = 0;
-        bool live = __any_sync(kFull, L.active);
-        for (; live && t + 2 <= K; t += 2) {
-            rasp_step<SC, CT, POW2, AR, false, true>(L, tb, lm, uend, yend, g, q, t, true);
-            rasp_step<SC, CT, POW2, AR, false, true>(L, tb, lm, uend, yend, g, q, t + 1, true);
-            live = __any_sync(kFull, L.active);
-        }
-        if (live && t < K) {
-            rasp_step<SC, CT, POW2, AR, false, true>(L, tb, lm, uend, yend, g, q, t, true);
-            ++t;
-            live = __any_sync(kFull, L.active);
-        }
-        if (live) rasp_step<SC, CT, POW2, AR, true, true>(L, tb, lm, uend, yend, g, q, K, false);
-
         uint64_t v = 0;
-        uint32_t halted = 1;
-        uint64_t my_steps = 0;
-        if (valid_x) {
-            halted = 1;
-            uint32_t tend = L.tlast;
-            if (L.active) {
-                halted = 0;            // cannot happen: the final evaluation classifies everyone
-            } else if (L.tlast == L.rem) {
-                const Fetch<CT> f = fetch<SC, CT, POW2, AR, true>(L, tb, lm, g, q);
-                halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, g, q) ? 1u : 0u;
+        bool all_halted = true;
+        for (uint32_t grp = 0; grp < groups; ++grp) {
+            const uint32_t x = grp * 32 + lane;               // the input word of this lane
+            const bool valid_x = x < xs;
+            // c0: every lane holds the same program, so the warp writes the
+            // M rows 16 bytes at a time (row k = 8 copies of cell k per 16 B)
+            for (uint32_t c = lane; c < 4 * n; c += 32) {
+                const uint32_t k = c >> 2;
+                uint32_t cell = 0;
+                if (k < 2 * A.m) {
+                    const uint32_t pair = static_cast<uint32_t>(r >> ((k >> 1) * pw)) & ((1u << pw) - 1u);
+                    cell = (k & 1) ? (pair >> A.ob) : (pair & ((1u << A.ob) - 1u));
+                }
+                const uint32_t w2 = cell | (cell << 16);
+                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(tile0 + k * ROW + (c & 3) * 16), "r"(w2)
+                             : "memory");
             }
-            const uint32_t y0 = (L.ya - Y) / ROW;
-            const uint32_t y1 = *reinterpret_cast<const SC *>(gb + Y);   // y[1] (0 unless written)
-            const uint64_t key = static_cast<uint64_t>(x) | (static_cast<uint64_t>(halted) << 8) |
-                                 (static_cast<uint64_t>(y0) << 9) |
-                                 (static_cast<uint64_t>(y0 ? y1 : 0u) << 10) |
-                                 (static_cast<uint64_t>(halted ? tend : 0u) << 18);
-            v = mix64(key);
-            my_steps = tend;
-        }
-        // block reduction: sum of v, AND of halted, sum of steps
-        for (int off = 16; off; off >>= 1) {
-            v += __shfl_down_sync(kFull, v, off);
-            my_steps += __shfl_down_sync(kFull, my_steps, off);
-        }
-        const unsigned all = __all_sync(kFull, halted != 0);
-        if (lane == 0) {
-            red_sum[wib] = v;
-            red_all[wib] = all;
-            red_steps[wib] = my_steps;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t sum = 0, st = 0;
-            unsigned a = 1;
-            for (uint32_t w2 = 0; w2 < (blockDim.x >> 5); ++w2) {
-                sum += red_sum[w2];
-                a &= red_all[w2];
-                st += red_steps[w2];
+            st_cell<SC, CT, true>(tb, U, x);   // u[1] = x
+            __syncwarp();
+            LaneState<CT> L;
+            L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tlast = 0; L.rem = A.tau;
+            L.active = true;
+            const uint32_t K = A.tau;
+            uint32_t t = 0;
+            bool live = true;
+            for (; live && t + 2 <= K; t += 2) {
+                rasp_step_free<SC, CT, POW2, AR, true>(L, tb, lm, uend, yend, g, q);
+                rasp_step_free<SC, CT, POW2, AR, true>(L, tb, lm, uend, yend, g, q);
+                live = __any_sync(kFull, valid_x & L.active);
             }
-            A.records[pi] = (static_cast<uint64_t>(a) << 63) | (sum & 0x7fffffffffffffffull);
-            atomicAdd(A.steps_total, static_cast<unsigned long long>(st));
+            if (live && t < K) {
+                rasp_step_free<SC, CT, POW2, AR, true>(L, tb, lm, uend, yend, g, q);
+                ++t;
+            }
+            if (valid_x) {
+                // tlast = moves: below K the machine stopped at a fixed point;
+                // at K it is fixed there or out of budget
+                bool halted = L.tlast < K;
+                if (!halted) {
+                    const Fetch<CT> f = fetch<SC, CT, POW2, AR, true>(L, tb, lm, g, q);
+                    halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, g, q);
+                }
+                const uint32_t y0 = (L.ya - Y) / ROW;
+                const uint32_t y1 = *reinterpret_cast<const SC *>(gb + Y);   // y[1] (0 unless written)
+                const uint64_t key = static_cast<uint64_t>(x) | (static_cast<uint64_t>(halted) << 8) |
+                                     (static_cast<uint64_t>(y0) << 9) |
+                                     (static_cast<uint64_t>(y0 ? y1 : 0u) << 10) |
+                                     (static_cast<uint64_t>(halted ? L.tlast : 0u) << 18);
+                v += mix64(key);
+                all_halted &= halted;
+                my_steps += L.tlast;
+            }
+            __syncwarp();   // the next group rewrites every column
         }
-        __syncthreads();
+        for (int off = 16; off; off >>= 1) v += __shfl_down_sync(kFull, v, off);
+        const unsigned all = __all_sync(kFull, all_halted);
+        if (lane == 0) A.records[pi] = (static_cast<uint64_t>(all != 0) << 63) | (v & 0x7fffffffffffffffull);
+    }
+    // machine-steps: one atomic per block
+    for (int off = 16; off; off >>= 1) my_steps += __shfl_down_sync(kFull, my_steps, off);
+    if (lane == 0) red_steps[wib] = my_steps;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long st = 0;
+        for (uint32_t w2 = 0; w2 < (blockDim.x >> 5); ++w2) st += red_steps[w2];
+        if (st) atomicAdd(A.steps_total, st);
     }
 }
 
