@@ -53,6 +53,12 @@ CONFIGS = {
     "paper": (1 << 20, 32, 250, 10, 2, 10000,
               "1M machines: 64 sampled+lowered L=30 programs (reference build_workload) x random "
               "inputs, w=32 n=250 l=10 s=2, tau 10^4"),
+    # SURVEY §8f f3 at the paper's own protocol: L=100 programs sampled and
+    # lowered by the reference (golden fixture paper100, 512 programs), tiled to
+    # 1M machines with fresh random inputs, tau_max 10^6
+    "paper6": (1 << 20, 32, 250, 10, 2, 10 ** 6,
+               "1M machines: 512 sampled+lowered L=100 programs (reference build_workload) x random "
+               "inputs, w=32 n=250 l=10 s=2, tau 10^6 (the paper protocol)"),
     # d = programs; machines = programs x 2^w inputs (SURVEY §8d C4 domain)
     "c4": (1 << 28, 8, 16, 1, 1, 64,
            "exhaustive: all 2^28 programs of m=4 pairs (3-bit opcode, 4-bit operand), w=8 n=16, "
@@ -132,16 +138,21 @@ class ClockSampler:
 def make_c0(cfg_name, d, p, seed):
     """Host c0 for a config: generator G, or the paper-protocol programs."""
     from paper_2604_12902_b200.workload import synthetic_c0
-    if cfg_name != "paper":
+    if cfg_name not in ("paper", "paper6"):
         return synthetic_c0(d, p, seed=seed)
-    z = np.load(os.path.join(ROOT, "tests", "golden", "paper.npz"))
+    fam = "paper" if cfg_name == "paper" else "paper100"
+    z = np.load(os.path.join(ROOT, "tests", "golden", f"{fam}.npz"))
     M0, u0 = z["g000_c0_M"].astype(np.uint32), z["g000_c0_u"].astype(np.uint32)
     reps = -(-d // M0.shape[0])
     M = np.tile(M0, (reps, 1))[:d]
     u = np.tile(u0, (reps, 1))[:d]
     rng = np.random.default_rng(seed)
     fresh = rng.integers(0, 1 << 32, u.shape, dtype=np.uint64).astype(np.uint32)
-    used = np.tile((u0 != 0), (reps, 1))[:d]
+    if "nin" in z.files:   # each program's own input count (sampler ast.n_in)
+        nin = np.tile(z["nin"], reps)[:d]
+        used = np.arange(u.shape[1])[None, :] <= nin[:, None]
+    else:                  # inputs the sampled configuration set
+        used = np.tile((u0 != 0), (reps, 1))[:d]
     used[:, 0] = False
     u = np.where(used, fresh, u)
     return {"iw": np.zeros(d, np.uint32), "ac": np.zeros(d, np.uint32), "M": np.ascontiguousarray(M),
@@ -173,6 +184,8 @@ def cpu_reference(cfg_name, steps_k, warmup, sample_d=None, seed=0):
                 f"{steps_total} machine-steps, {cores} threads, best of {len(times)}",
                 "seconds": best}
     sample = min(d, sample_d or (1 << 20))
+    if cfg_name == "paper6":   # ~2.2e5 machine-steps per machine: keep the sample to seconds
+        sample = min(sample, 8192)
     p = MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
     c0 = make_c0(cfg_name, sample, p, seed)
     for it in range(warmup + steps_k):
@@ -184,9 +197,10 @@ def cpu_reference(cfg_name, steps_k, warmup, sample_d=None, seed=0):
             steps_total = int(out["steps"].sum())
     best = min(times) if times else float("nan")
     return {"value": steps_total / best, "unit": "machine-steps/s", "cores": cores,
-            "kind": "port", "sample": f"{sample} machines of {cfg_name} (generator G seed {seed}), "
+            "kind": "port", "sample": f"{sample} machines of {cfg_name} "
+            f"({'reference-sampled programs' if cfg_name.startswith('paper') else 'generator G'} seed {seed}), "
             f"{steps_total} machine-steps, _worker semantics, W={cores} threads, q=64, "
-            f"best of {len(times)}", "seconds": best}
+            f"best of {len(times)}", "seconds": best, "d_sample": sample}
 
 
 def bench_enumeration(args, world, rank, dev, desc):
@@ -278,7 +292,7 @@ def bench_enumeration(args, world, rank, dev, desc):
         dist.destroy_process_group()
 
 
-DEFAULT_EPOCH = {"c1": 64, "c2": 48, "c3": 48, "c5": 256, "paper": 32}
+DEFAULT_EPOCH = {"c1": 64, "c2": 48, "c3": 48, "c5": 256, "paper": 32, "paper6": 32}
 
 
 def main():
@@ -322,10 +336,11 @@ def main():
             "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "u64",
             "data": {"c4": "exhaustive enumeration",
-                     "paper": "reference-sampled programs x random inputs"}.get(args.config,
+                     "paper": "reference-sampled programs x random inputs",
+                     "paper6": "reference-sampled programs x random inputs"}.get(args.config,
                                                                               "synthetic (generator G)"),
             "config": {"workload": args.config, "desc": desc, "w": w, "n": n, "ell": ell, "s": s,
-                       "tau_max": tau, "d_sample": min(d, args.cpu_sample)},
+                       "tau_max": tau, "d_sample": cb.get("d_sample", min(d, args.cpu_sample))},
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": "machine-steps/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
@@ -482,8 +497,9 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": t_step * 1e3,
         "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
         "dtype": "u16" if w <= 16 else "u32",
-        "data": ("64 reference-sampled L=30 programs x random inputs (seed = rank)" if args.config == "paper"
-                 else "synthetic (generator G, SURVEY §8d; seed = rank)"),
+        "data": {"paper": "64 reference-sampled L=30 programs x random inputs (seed = rank)",
+                 "paper6": "512 reference-sampled L=100 programs x random inputs (seed = rank)"}.get(
+                     args.config, "synthetic (generator G, SURVEY §8d; seed = rank)"),
         "config": {"workload": args.config, "desc": desc, "d_per_gpu": d, "w": w, "n": n,
                    "ell": ell, "s": s, "tau_max": tau, "epoch": args.epoch,
                    "machine_steps_per_gpu": machine_steps, "halted_frac": total_halted / (d * world),

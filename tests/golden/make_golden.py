@@ -20,6 +20,9 @@ final iw/ac/M/u/y, status, steps, tau_h.  Families:
   bb      the three Appendix-B busy-beaver fixtures lowered at p32
           (tests/test_lowering.py:179-187: tau_h 1727/1409/1387, y=(1,0))
   paper   build_workload(30, 64, seed=3, p32) (hypervisor.py:362-384), tau 10^4
+  paper100  build_workload(100, 512, seed=5, p32): the paper protocol's program
+          length L=100 at its tau_max = 10^6; `nin` holds
+          each program's input count (sampler ast.n_in)
   gen_*   generator G at C1 (4096, w8 n32 l4 s4, 64 steps) and
           small samples of the C2 and C5 shapes at cap 1024
 
@@ -231,6 +234,15 @@ def fam_paper():
     f.save()
 
 
+def fam_paper100():
+    f = Family("paper100")
+    p32 = RM.MachineParams(w=32, n=250, ell=10, s=2, mu=10)
+    wl = H.build_workload(100, 512, 5, p32, keep_asts=True)
+    f.add(p32, 10 ** 6, _arrays(wl.configs, p32))
+    f.data["nin"] = np.array([a.n_in for a in wl.asts], np.int64)
+    f.save()
+
+
 def fam_gen():
     f = Family("gen")
     for d, (w, n, ell, s), tau in ((4096, (8, 32, 4, 4), 64),
@@ -242,7 +254,11 @@ def fam_gen():
     f.save()
 
 
+ALL = (fam_kat, fam_edge, fam_corpus, fam_hyp, fam_bb, fam_paper, fam_paper100, fam_gen)
+
 if __name__ == "__main__":
     H._warm_kernel()
-    for fam in (fam_kat, fam_edge, fam_corpus, fam_hyp, fam_bb, fam_paper, fam_gen):
-        fam()
+    only = set(sys.argv[1:])   # optional family names
+    for fam in ALL:
+        if not only or fam.__name__[4:] in only:
+            fam()

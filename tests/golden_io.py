@@ -8,7 +8,7 @@ from dataclasses import dataclass
 import numpy as np
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
-FAMILIES = ("kat", "edge", "corpus", "hyp", "bb", "paper", "gen")
+FAMILIES = ("kat", "edge", "corpus", "hyp", "bb", "paper", "paper100", "gen")
 FIELDS = ("iw", "ac", "M", "u", "y")
 RESULTS = FIELDS + ("status", "steps", "tau_h")
 
