@@ -170,6 +170,9 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
         pl.warps_per_block = c.wpb;
         pl.dyn_smem = pl.tile_bytes * size_t(c.wpb);
         pl.blocks = c.per_sm * dv.nsm;
+        if (std::getenv("RASP_DEBUG"))   // plan of this launch sequence (tuning aid)
+            std::fprintf(stderr, "rasp: tile %zu B (%u rows), %d warps/block, %d blocks/SM, big %d\n",
+                         pl.tile_bytes, pl.tile_rows, c.wpb, c.per_sm, int(BIG));
     }
     const int threads = 32 * pl.warps_per_block;
     const uint64_t tiles = (d + 31) / 32;
