@@ -296,3 +296,36 @@ def test_run_programs_host_path(pkg):
     with pytest.raises(ValueError):
         H.run_programs(np.full((4, 2), 70000, np.uint32), np.zeros((4, 1), np.uint32), p,
                        H.BatchConfig(tau_max=1))
+
+
+def test_cuda_graph_replay_matches_eager(pkg):
+    """rasp_run + rasp_histogram captured in a CUDA graph (what bench.py times)
+    and replayed give the eager results: the launch sequence is fixed and
+    everything is enqueued on the caller's stream."""
+    import torch
+    P, H = pkg
+    from paper_2604_12902_b200.engine import DeviceBatch
+    from paper_2604_12902_b200.workload import synthetic_c0
+    p = P.MachineParams(w=16, n=64, ell=8, s=8, mu=1)
+    dev = torch.device("cuda:0")
+    src = DeviceBatch.from_arrays(synthetic_c0(50_000, p, seed=9), p, dev)
+    eng = H.get_engine(p, dev)
+    ref = DeviceBatch.empty(src.d, p, dev, fresh=False)
+    eng.run(src, 1024, 48, out=ref, fresh=True)
+    href = eng.histogram(ref).clone()
+    dst = DeviceBatch.empty(src.d, p, dev, fresh=False)
+    hist = torch.empty(102, dtype=torch.int64, device=dev)
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cap):
+        eng.run(src, 1024, 48, out=dst, fresh=True, stream=cap)
+        eng.histogram(dst, out=hist, stream=cap)
+    for _ in range(2):
+        for t in (dst.iw, dst.M, dst.steps):
+            t.zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for k in ("iw", "ac", "M", "u", "y", "status", "steps", "tau_h"):
+            assert torch.equal(getattr(dst, k), getattr(ref, k)), k
+        assert torch.equal(hist, href)
