@@ -502,20 +502,23 @@ def main():
     bytes_alg = d * 2 * s_alg_bytes(w, n, ell, s)          # per GPU, per launch set
     issue_peak = 148 * 4 * 32 * sm_mhz * 1e6                 # thread-instr/s
     ach_issue = machine_steps * N_ALG_INSTR / t_kernel
-    traffic = None
+    # measured DRAM bytes of the epoch kernels per run (ncu capture committed
+    # under profiles/; bytes per launch set, like `achieved`)
+    traffic, traffic_detail = None, None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             tr = json.load(f).get(args.config)
         if tr:
-            traffic = {"bytes_per_run": tr["bytes_per_run"],
-                       "vs_algorithmic": tr["bytes_per_run"] / tr["algorithmic_bytes_per_run"],
-                       "source": tr["source"]}
+            traffic = tr["bytes_per_run"]
+            traffic_detail = {"unit": "bytes per run (dram__bytes_read.sum + dram__bytes_write.sum)",
+                              "vs_algorithmic": tr["bytes_per_run"] / tr["algorithmic_bytes_per_run"],
+                              "source": tr["source"]}
     except (OSError, ValueError, KeyError):
         pass
     roof = {
         "bound": "issue", "unit": "Tinstr/s",
         "achieved": ach_issue / 1e12, "peak": issue_peak / 1e12,
-        "frac": ach_issue / issue_peak, "traffic": traffic,
+        "frac": ach_issue / issue_peak, "traffic": traffic, "traffic_detail": traffic_detail,
         "per_unit": f"{N_ALG_INSTR} int-instr per machine-step (SURVEY §8d)",
         "peak_source": f"148 SM x 128 lanes x {sm_mhz:.0f} MHz ({peak_kind} sm_max_mhz)",
         "hbm": {"achieved": bytes_alg / t_kernel / 1e9, "peak": hbm_gbs, "unit": "GB/s",
