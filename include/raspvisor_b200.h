@@ -91,7 +91,9 @@ size_t rasp_workspace_bytes(const rasp_params *p, uint64_t d);
  *             epochs double it.  Performance knob only.
  *   workspace: device buffer of at least rasp_workspace_bytes(p, d) bytes.
  * Asynchronous on `stream` (may synchronise internally only when tau_max is
- * too large for a fixed epoch schedule, to poll the live count). */
+ * too large for a fixed epoch schedule, to poll the live count).  A machine
+ * can run at most 1024 epochs of at most 2^24 steps (~1.7e10 steps): larger
+ * budgets on machines that never halt return RASP_ECAPACITY. */
 int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out,
              int64_t tau_max, int64_t epoch, uint32_t flags,
              void *workspace, size_t workspace_bytes, void *stream);

@@ -33,6 +33,18 @@ inline int cuda_fail(cudaError_t e, const char *what)
 using rasp::kMaxEpochs;                 // schedule slots in the workspace
 constexpr int kPollAfter = 24;          // epochs after which the host polls the schedule
 constexpr uint32_t kMaxK = 1u << 24;    // longest epoch, in steps
+
+// Longest epoch actually used: kMaxK, or $RASP_KMAX (tests shorten it to drive
+// long budgets through the host's polling path with small tau_max).
+inline uint32_t max_epoch_len()
+{
+    static const uint32_t v = [] {
+        const char *e = std::getenv("RASP_KMAX");
+        const unsigned long x = e ? std::strtoul(e, nullptr, 10) : 0ul;
+        return x >= 1 && x <= kMaxK ? uint32_t(x) : kMaxK;
+    }();
+    return v;
+}
 constexpr int kWarpsPerBlockMax = 4;
 constexpr size_t kBigTile = 16 * 1024;  // tiles above this use the one-warp, many-register kernel
 constexpr size_t kGlobalTileBudget = size_t(1) << 30;  // bytes of HBM tiles for huge n
@@ -182,13 +194,14 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
     RASP_CUDA(cudaMemsetAsync(ws.sched, 0, sizeof(rasp::Sched), st));
     // Enough launches for the pure doubling schedule; the device schedule can
     // only finish sooner (it lengthens epochs once survivors stop halting).
-    const uint64_t K0 = uint64_t(std::min<int64_t>(std::max<int64_t>(epoch, 1), tau_max));
+    const uint64_t K0 = std::min<uint64_t>(uint64_t(std::min<int64_t>(std::max<int64_t>(epoch, 1), tau_max)),
+                                           max_epoch_len());
     int planned = 1;
     bool covers = int64_t(K0) >= tau_max;
     {
         uint64_t cov = K0, k = std::max<uint64_t>(K0, 1);
         while (int64_t(cov) < tau_max && planned < kPollAfter) {
-            k = std::min<uint64_t>(k * 2, kMaxK);
+            k = std::min<uint64_t>(k * 2, max_epoch_len());
             cov += k;
             ++planned;
         }
@@ -210,7 +223,7 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
         a.first = e == 0;
         a.count_in = uint32_t(d);
         a.K0 = uint32_t(K0);
-        a.kmax = kMaxK;
+        a.kmax = max_epoch_len();
         a.list_in = e == 0 ? nullptr : ws.lists[(e - 1) & 1];
         a.list_out = ws.lists[e & 1];
         kern<<<grid, threads, pl.dyn_smem, st>>>(a, static_cast<SC *>(ws.gtiles));

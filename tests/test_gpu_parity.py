@@ -329,3 +329,44 @@ def test_cuda_graph_replay_matches_eager(pkg):
         for k in ("iw", "ac", "M", "u", "y", "status", "steps", "tau_h"):
             assert torch.equal(getattr(dst, k), getattr(ref, k)), k
         assert torch.equal(hist, href)
+
+
+_LONG_BUDGET = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+from oracle import oracle
+from paper_2604_12902_b200 import hypervisor as H
+from paper_2604_12902_b200.machine import MachineParams
+from paper_2604_12902_b200.workload import random_configs
+p = MachineParams(w=16, n=16, ell=3, s=3, mu=1)
+c0 = random_configs(4096, p, np.random.default_rng(5))
+# a third of the machines loop forever: LOD 1 ; BNZ 0 (i cycles 0 -> 2 -> 0)
+loop = np.zeros(16, np.uint16); loop[:4] = (1, 1, 5, 0)
+c0["M"][::3] = loop; c0["iw"][::3] = 0
+tau = 20000
+want = oracle.worker_arrays(c0, 16, 16, 3, 3, tau)
+for epoch in (1, 50):
+    res = H.run_arrays(c0, p, H.BatchConfig(tau_max=tau, epoch=epoch))
+    for k in ("iw", "ac", "M", "u", "y", "status", "steps", "tau_h"):
+        got = np.asarray(getattr(res.slots, k))
+        if k in ("iw", "ac", "M", "u", "y"):
+            got = got.astype(np.uint64)
+        assert np.array_equal(got, want[k]), (epoch, k)
+print("ok")
+"""
+
+
+def test_long_budget_polling_path(pkg, tmp_path):
+    """Budgets beyond what the pre-planned launches cover: the host polls the
+    device schedule for more epochs.  RASP_KMAX shortens the longest epoch so
+    tau = 20000 needs ~80 of them (the planned launches cover 24)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "long_budget.py"
+    script.write_text(_LONG_BUDGET)
+    env = dict(os.environ, RASP_KMAX="256")
+    out = subprocess.run([sys.executable, str(script), root], env=env, capture_output=True, text=True,
+                         timeout=300)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
