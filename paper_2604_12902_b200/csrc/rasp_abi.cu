@@ -91,11 +91,16 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     if (const char *e = std::getenv("RASP_PREFETCH")) a.pf_dist = uint32_t(std::strtoul(e, nullptr, 10));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     if (!a.inplace) {
-        // out-of-place: the input tapes and the bookkeeping arrays move in bulk;
-        // the kernels then treat `out` as the working copy
-        const size_t ub = size_t(d) * (p->ell + 1) * wb, yb = size_t(d) * (p->s + 1) * wb;
-        int rc2 = dev_copy(out->u, in->u, ub, dv, st);
-        if (!rc2) rc2 = dev_copy(out->y, in->y, yb, dv, st);
+        // out-of-place: the bookkeeping arrays move in bulk (non-fresh runs);
+        // u and y rows are copied by the first epoch, tile by tile (bulk
+        // copies here for big tiles); the kernels then treat `out` as the
+        // working copy
+        int rc2 = RASP_OK;
+        if (pl.smem && pl.big) {
+            const size_t ub = size_t(d) * (p->ell + 1) * wb, yb = size_t(d) * (p->s + 1) * wb;
+            rc2 = dev_copy(out->u, in->u, ub, dv, st);
+            if (!rc2) rc2 = dev_copy(out->y, in->y, yb, dv, st);
+        }
         if (!rc2 && !a.fresh) {
             rc2 = dev_copy(out->status, in->status, size_t(d), dv, st);
             if (!rc2) rc2 = dev_copy(out->steps, in->steps, size_t(d) * 8, dv, st);

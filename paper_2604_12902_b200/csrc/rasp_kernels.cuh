@@ -392,6 +392,23 @@ __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes)
                  : "memory");
 }
 
+
+// Warp-cooperative copy of a contiguous byte range (16-byte vectors when both
+// ends allow it).
+__device__ __forceinline__ void warp_copy(void *dst, const void *src, uint64_t bytes, uint32_t lane)
+{
+    const uintptr_t a = reinterpret_cast<uintptr_t>(dst) | reinterpret_cast<uintptr_t>(src);
+    uint64_t k0 = 0;
+    if ((a & 15) == 0) {
+        const uint64_t n16 = bytes >> 4;
+        for (uint64_t k = lane; k < n16; k += 32)
+            reinterpret_cast<uint4 *>(dst)[k] = reinterpret_cast<const uint4 *>(src)[k];
+        k0 = n16 << 4;
+    }
+    for (uint64_t k = k0 + lane; k < bytes; k += 32)
+        static_cast<unsigned char *>(dst)[k] = static_cast<const unsigned char *>(src)[k];
+}
+
 // --- one machine per lane -------------------------------------------------------
 //
 // Tile layout per warp: row r holds cell r of all 32 lanes (SC each).
@@ -861,6 +878,19 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const Side &dst = A.out;
             const uint64_t ucols = static_cast<uint64_t>(A.g.ell) + 1;
             const uint64_t ycols = static_cast<uint64_t>(A.g.s) + 1;
+            if (copy_side && !BIG) {
+                // out-of-place first epoch: the tile's machines are contiguous
+                // (identity list), so their u and y rows are two contiguous
+                // blocks -- copy them to `out` here, before any write-back of
+                // this tile touches them (replaces a bulk copy kernel per tape;
+                // the latency-bound big tiles keep the bulk copies: measured)
+                const uint64_t m0 = static_cast<uint64_t>(tix) * 32;
+                const uint64_t m1 = min(static_cast<uint64_t>(count), m0 + 32);
+                warp_copy(static_cast<S *>(dst.u) + m0 * ucols, static_cast<const S *>(A.in.u) + m0 * ucols,
+                          (m1 - m0) * ucols * sizeof(S), lane);
+                warp_copy(static_cast<S *>(dst.y) + m0 * ycols, static_cast<const S *>(A.in.y) + m0 * ycols,
+                          (m1 - m0) * ycols * sizeof(S), lane);
+            }
             const uint32_t j = tix * 32 + lane;
             const bool valid = j < count;
             const uint64_t id = valid ? (A.list_in ? A.list_in[j] : j) : 0;
@@ -876,8 +906,8 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const S *srcU = static_cast<const S *>(src.u) + id * ucols;
             const S *srcY = static_cast<const S *>(src.y) + id * ycols;
             if (valid && copy_side && !running) {
-                // untouched machine, out-of-place: carry i, a, M over (u, y were
-                // copied in bulk by the host)
+                // untouched machine, out-of-place: carry i, a, M over (u, y are
+                // copied per tile above, or in bulk by the host for big tiles)
                 static_cast<S *>(dst.iw)[id] = static_cast<const S *>(A.in.iw)[id];
                 static_cast<S *>(dst.ac)[id] = static_cast<const S *>(A.in.ac)[id];
                 copy_cells(static_cast<S *>(dst.M) + id * n, srcM, n);
