@@ -6,10 +6,11 @@ Workload (BASELINE.json configs[1]): per GPU, 2^20 synthetic
 programs from generator G (seed = rank), w=16, n=64, ell=8, s=8, run to halt
 with a 1024-step cap.  Each rank runs its own shard (weak scaling; no
 collective on the data path -- after the run the 102-bucket halting
-histogram is all-reduced and rank 0 gathers every shard's verdicts and
-output tapes over NCCL).  --config c3 is BASELINE configs[2]: 16M machines in
-total split across the ranks (strong scaling); c1 and c5 are configs[0] and
-configs[4].
+histogram, i.e. the halt counts, is all-reduced over NCCL and every shard's
+results stay on its GPU).  --config c3 is BASELINE configs[2]: 16M machines
+in total split across the ranks (strong scaling) with the output gather of
+that config: rank 0 gathers every shard's verdicts and output tapes over
+NCCL (--gather on|off overrides); c1 and c5 are configs[0] and configs[4].
 
 One "step" = one full run of the batch from c0 (out-of-place, c0 is never
 modified) plus the on-device halting histogram.  Metric: machine-steps/s
@@ -312,6 +313,8 @@ def main():
     ap.add_argument("--cpu-sample", type=int, default=1 << 20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-graph", action="store_true", help="time eager launches instead of graph replays")
+    ap.add_argument("--gather", choices=("auto", "on", "off"), default="auto",
+                    help="N > 1: gather verdicts and output tapes to rank 0 every step (auto: c3 only)")
     args = ap.parse_args()
     if args.epoch is None:
         args.epoch = DEFAULT_EPOCH.get(args.config, 64)
@@ -377,8 +380,10 @@ def main():
     stream = torch.cuda.current_stream(dev)
 
     # N > 1: rank 0 gathers every shard's verdicts and output tapes
+    # where the config asks for it (c3: "output gather via NCCL")
+    do_gather = world > 1 and (args.gather == "on" or (args.gather == "auto" and args.config == "c3"))
     gathers = []
-    if world > 1:
+    if do_gather:
         for t in (dst.status, dst.steps, dst.tau_h, dst.y.view(torch.uint8)):
             gathers.append((t, [torch.empty_like(t) for _ in range(world)] if rank == 0 else None))
 
@@ -541,7 +546,8 @@ def main():
                    "l2": "flushed between steps (256 MB write, outside the events)",
                    "launch": "CUDA graph replay of rasp_run + histogram" if graph is not None else
                              ("eager launches" + (f" ({graph_note})" if graph_note else "")),
-                   "parallelism": (f"{world} contiguous shards, NCCL all-reduce(histogram) + gather(verdicts, y)"
+                   "parallelism": (f"{world} contiguous shards, NCCL all-reduce(histogram)"
+                                   + (" + gather(verdicts, y) to rank 0" if do_gather else "")
                                    if world > 1 else "1 GPU")},
         "programs_per_s": d * world / t_step,
         "e2e": {"value": total_steps / t_e2e, "unit": "machine-steps/s",
