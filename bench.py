@@ -476,7 +476,11 @@ def main():
     # the reference's inputs are programs and input words (build_workload ->
     # init_config, hv:362-384): copy those in, assemble c0 on the device
     pipe = HostPipeline(p, d, dev, engine=eng)
-    pin_in = pipe.pinned_programs(host["M"], host["u"][:, 1:])
+    # programs are passed at the longest program's length L (init_config pads
+    # memory with zeros, m:289-309); generator G programs fill memory (L = n)
+    nz = np.flatnonzero(host["M"].any(axis=0))
+    L = int(nz[-1]) + 1 if nz.size else 1
+    pin_in = pipe.pinned_programs(host["M"][:, :L], host["u"][:, 1:])
     e2e_times = []
     for it in range(args.warmup + args.steps):
         t = pipe.run_programs(pin_in, tau, args.epoch)
