@@ -370,3 +370,26 @@ def test_long_budget_polling_path(pkg, tmp_path):
     out = subprocess.run([sys.executable, str(script), root], env=env, capture_output=True, text=True,
                          timeout=300)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+@pytest.mark.parametrize("shape", [(32, 2048, 4, 2), (16, 4096, 4, 2), (16, 3000, 3, 3), (64, 1200, 2, 2)])
+def test_huge_memory_hbm_tiles(pkg, shape):
+    """n so large that a warp's tile exceeds shared memory: the kernel keeps
+    the tiles in HBM (the generic path, gated steps)."""
+    P, H = pkg
+    from oracle import oracle
+    from paper_2604_12902_b200.workload import random_configs
+    w, n, ell, s = shape
+    p = P.MachineParams(w=w, n=n, ell=ell, s=s, mu=1)
+    c0 = random_configs(1024, p, np.random.default_rng(n))
+    # a few long runners: a LOD/BNZ loop at the start of memory
+    c0["M"][::7, :4] = np.array([1, 1, 5, 0], dtype=c0["M"].dtype)
+    c0["iw"][::7] = 0
+    for tau in (0, 300):
+        want = oracle.worker_arrays(c0, w, n, ell, s, tau)
+        res = H.run_arrays(c0, p, H.BatchConfig(tau_max=tau, epoch=16, memory_budget_words=1 << 40))
+        for k in RESULTS:
+            got = np.asarray(getattr(res.slots, k))
+            if k in FIELDS:
+                got = got.astype(np.uint64)
+            np.testing.assert_array_equal(got, want[k], err_msg=f"{shape} tau={tau} {k}")
