@@ -8,8 +8,8 @@ dev = torch.device("cuda", 0)
 p = MachineParams(w=16, n=64, ell=8, s=8, mu=1)
 d = 1 << 20
 host = synthetic_c0(d, p, seed=0)
-for chunks in (2, 3, 4, 6, 8, 12, 16):
+for chunks in (4, 6, 8, 12, 16, 24, 32):
     pipe = HostPipeline(p, d, dev, chunks=chunks)
     pin = pipe.pinned_programs(host["M"], host["u"][:, 1:])
-    ts = sorted(pipe.run_programs(pin, 1024, 64) for _ in range(6))
+    ts = sorted(pipe.run_programs(pin, 1024, 48) for _ in range(6))
     print(f"chunks={chunks}: best {ts[0]*1e3:.2f} median {ts[3]*1e3:.2f} ms")
