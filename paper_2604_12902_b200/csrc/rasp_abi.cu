@@ -82,9 +82,6 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.fresh = (flags & RASP_FRESH) ? 1 : 0;
     a.inplace = (in->iw == out->iw) ? 1 : 0;
     a.tile_rows = pl.tile_rows;
-    a.one = 1;
-    a.two = 2;
-    a.row = uint32_t(32 * cell_bytes(p->w));
     a.stable_q8 = 128;                       // 0.5 (measured best on C2 and C5): tuning knob RASP_STABLE_Q8
     if (const char *e = std::getenv("RASP_STABLE_Q8")) a.stable_q8 = uint32_t(std::strtoul(e, nullptr, 10));
     a.pf_dist = 1;                           // tuning knob RASP_PREFETCH (0 disables)
@@ -146,9 +143,6 @@ int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t cou
     a.ob = ep->opcode_bits;
     a.pb = ep->operand_bits;
     a.tau = ep->tau_max;
-    a.one = 1;
-    a.two = 2;
-    a.row = 64;
     const size_t smem = size_t(8) * (ep->n + 3) * 64;
     const bool pow2 = (ep->n & (ep->n - 1)) == 0;
     auto kern = pow2 ? rasp::enum_kernel<true, rasp::Arith::NARROW> : rasp::enum_kernel<false, rasp::Arith::NARROW>;

@@ -91,8 +91,6 @@ struct EpochArgs {
     uint32_t fresh;                // status=0, steps=0, tau_h=-1 on input
     uint32_t inplace;              // in == out
     uint32_t tile_rows;            // n + ell + 1 (+ s output rows unless BIG)
-    uint32_t one, two;             // the constants 1 and 2 (see Opq)
-    uint32_t row;                  // bytes per tile row (32 * sizeof(SC))
     uint32_t stable_q8;            // survival ratio (x256) at which the rest runs as one epoch
     uint32_t pf_dist;              // L2 prefetch distance in rounds of resident warps (0: off)
 };
@@ -1144,7 +1142,6 @@ struct EnumArgs {
     unsigned long long *steps_total;
     uint32_t m, ob, pb;      // pairs, opcode bits, operand bits
     uint32_t tau;            // step budget
-    uint32_t one, two, row;
 };
 
 __device__ __forceinline__ uint64_t mix64(uint64_t z)
