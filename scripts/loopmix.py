@@ -19,7 +19,8 @@ for a, t in ins:
     if m and int(m.group(1), 16) < a:
         body = [x for x in ins if int(m.group(1), 16) <= x[0] <= a]
         nlds = sum(1 for x in body if "LDS" in x[1])
-        if any("VOTE" in x[1] for x in body) and nlds >= 16 and not any("LDG" in x[1] for x in body):
+        nldg = sum(1 for x in body if "LDG" in x[1])
+        if any("VOTE" in x[1] for x in body) and nlds >= 16 and nldg <= nlds:
             if best is None or len(body) < len(best):
                 best = body
 c = Counter((x[1].split()[1] if x[1].startswith("@") else x[1].split()[0]).split(".")[0] for x in best)
