@@ -19,7 +19,7 @@ from .machine import MachineParams
 
 class HostPipeline:
     def __init__(self, params: MachineParams, d: int, device=None, chunks: int = 8,
-                 engine: Engine | None = None, word_bytes: int | None = None):
+                 engine: Engine | None = None, word_bytes: int | None = None, small_groups: int = 4):
         self.params = params
         self.d = d
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -42,6 +42,10 @@ class HostPipeline:
         self.s_out = torch.cuda.Stream(self.device)
         self.h2d_bytes = 0
         self.d2h_bytes = sum(t.numel() * t.element_size() for t in self.host_out.values())
+        # copy-out: M (the bulk) per chunk; the small per-machine fields in a
+        # few large copies -- each copy costs ~10 us of PCIe time, and 8 fields
+        # x chunks of them cost more than the overlap wins (scripts/pcie_split.py)
+        self.small_groups = max(1, min(small_groups, len(self.bounds)))
         # one workspace per in-flight run (runs are serial on s_run, so one suffices)
         self.engine.workspace(max((b - a for a, b in self.bounds), default=0))
 
@@ -71,7 +75,7 @@ class HostPipeline:
         e0.record(main)
         for s in (self.s_in, self.s_run, self.s_out):
             s.wait_event(e0)
-        for a, b in self.bounds:
+        for c, (a, b) in enumerate(self.bounds):
             with torch.cuda.stream(self.s_in):
                 for k in WORD_FIELDS:
                     getattr(self.dev, k)[a:b].copy_(pinned[k][a:b], non_blocking=True)
@@ -83,9 +87,7 @@ class HostPipeline:
             ev_run = torch.cuda.Event()
             ev_run.record(self.s_run)
             self.s_out.wait_event(ev_run)
-            with torch.cuda.stream(self.s_out):
-                for k in ALL_FIELDS:
-                    self.host_out[k][a:b].copy_(getattr(self.dev, k)[a:b], non_blocking=True)
+            self._copy_out(c, a, b)
         main.wait_stream(self.s_out)
         e1.record(main)
         e1.synchronize()
@@ -122,7 +124,7 @@ class HostPipeline:
         for s in (self.s_in, self.s_run, self.s_out):
             s.wait_event(e0)
         P, X = self._stage["programs"], self._stage["inputs"]
-        for a, b in self.bounds:
+        for c, (a, b) in enumerate(self.bounds):
             with torch.cuda.stream(self.s_in):
                 P[a:b].copy_(pinned["programs"][a:b], non_blocking=True)
                 if X.shape[1]:
@@ -136,13 +138,23 @@ class HostPipeline:
             ev_run = torch.cuda.Event()
             ev_run.record(self.s_run)
             self.s_out.wait_event(ev_run)
-            with torch.cuda.stream(self.s_out):
-                for k in ALL_FIELDS:
-                    self.host_out[k][a:b].copy_(getattr(self.dev, k)[a:b], non_blocking=True)
+            self._copy_out(c, a, b)
         main.wait_stream(self.s_out)
         e1.record(main)
         e1.synchronize()
         return e0.elapsed_time(e1) / 1e3
+
+    def _copy_out(self, c: int, a: int, b: int) -> None:
+        """After chunk c = rows [a, b) has run: its M rows now, the small
+        fields of every finished chunk at the end of each group of chunks."""
+        with torch.cuda.stream(self.s_out):
+            self.host_out["M"][a:b].copy_(self.dev.M[a:b], non_blocking=True)
+            per = -(-len(self.bounds) // self.small_groups)
+            if (c + 1) % per == 0 or c + 1 == len(self.bounds):
+                lo = self.bounds[(c // per) * per][0]
+                for k in ALL_FIELDS:
+                    if k != "M":
+                        self.host_out[k][lo:b].copy_(getattr(self.dev, k)[lo:b], non_blocking=True)
 
     def results(self) -> dict:
         return {k: v.numpy() for k, v in self.host_out.items()}
