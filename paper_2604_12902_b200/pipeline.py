@@ -19,7 +19,8 @@ from .machine import MachineParams
 
 class HostPipeline:
     def __init__(self, params: MachineParams, d: int, device=None, chunks: int = 8,
-                 engine: Engine | None = None, word_bytes: int | None = None, small_groups: int = 4):
+                 engine: Engine | None = None, word_bytes: int | None = None, small_groups: int = 4,
+                 ramp: bool = True):
         self.params = params
         self.d = d
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -30,6 +31,11 @@ class HostPipeline:
         self.chunks = max(1, min(chunks, (d + 4095) // 4096))
         step = (d + self.chunks - 1) // self.chunks
         self.bounds = [(a, min(d, a + step)) for a in range(0, d, step)] if d else []
+        if ramp and self.chunks >= 4 and d >= 1 << 16:
+            # short first and last chunks: the pipeline fills and drains sooner
+            w = [1, 2] + [4] * (self.chunks - 4) + [2, 1]
+            cuts = np.cumsum([0] + w) * d // sum(w)
+            self.bounds = [(int(cuts[k]), int(cuts[k + 1])) for k in range(len(w))]
         wd = TORCH_WORD[self.wb]
         shapes = {"iw": (d,), "ac": (d,), "M": (d, params.n), "u": (d, params.ell + 1),
                   "y": (d, params.s + 1)}
