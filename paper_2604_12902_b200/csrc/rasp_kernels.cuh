@@ -840,7 +840,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     constexpr bool MX = SMEM && kMx<SC> && !BIG;
     // ungated steps with move counting (every lane's budget covers the epoch;
     // issue-bound shared-memory tiles -- big tiles keep the explicit form)
-    constexpr bool kCount = !BUDGET && AR != Arith::W1 && !BIG;
+    constexpr bool kCount = !BUDGET && AR != Arith::W1 && (!BIG || !POW2);
     // ungated steps with carried residues (n not a power of two)
     constexpr bool kInc = !BUDGET && AR != Arith::W1 && !POW2 && SMEM;
     constexpr uint32_t kUnroll = RASP_UNROLL;
