@@ -656,54 +656,6 @@ __device__ __forceinline__ void rasp_step_free(LaneState<CT> &L, char *base, uin
     L.i = ni;
 }
 
-// The explicit form of the ungated step (active &= !fixed; tlast = t while
-// live): the big-tile kernels, latency- rather than issue-bound, run faster
-// with it.
-template <class SC, class CT, bool POW2, Arith AR, bool SMEM, bool YG = false, class YS = SC>
-__device__ __forceinline__ void rasp_step_free_t(LaneState<CT> &L, char *base, uint32_t lm, uint32_t uend,
-                                               uint32_t yend, const Geo &g, const Opq &q, uint32_t t,
-                                               char *ybase = nullptr)
-{
-    static_assert(AR != Arith::W1, "w = 1 uses the gated step");
-    const CT mask = static_cast<CT>(g.mask);
-    const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, base, lm, g, q);
-    const CT a0 = L.a;
-    const bool ucap = L.ua >= uend;
-    const bool taken = (f.o == 5) & ((AR == Arith::CELL ? (a0 & mask) : a0) != 0);
-    bool self;
-    if constexpr (kRawI<POW2, AR> && AR != Arith::FULL) self = ((L.i ^ f.jw) & mask) == 0;
-    else self = f.jw == L.i;
-    const bool stay = (static_cast<CT>(f.o - 1) > 6) | ((f.o == 6) & ucap);   // i does not move
-    const bool fixed = stay | (taken & self);
-    if (L.active) L.tlast = t;
-    L.active = L.active & !fixed;
-    if (f.o == 1) L.a = f.jw;
-    if constexpr (AR == Arith::CELL) {
-        if (f.o == 2) L.a = a0 + f.mj;
-        if (f.o == 3) L.a = a0 * f.mj;
-    } else {
-        if (f.o == 2) L.a = wrap<CT, AR>(a0 + f.mj, mask);
-        if (f.o == 3) L.a = wrap<CT, AR>(a0 * f.mj, mask);
-    }
-    if (f.o == 4) st_cell<SC, CT, SMEM>(base, f.jo, a0);
-    if ((f.o == 6) & !ucap) {
-        st_cell<SC, CT, SMEM>(base, f.jo, f.ud);
-        L.ua += q.row;
-    }
-    if constexpr (YG) {   // HBM row: lanes without a machine (no ybase) must not store
-        if (L.active & (f.o == 7) & (L.ya < yend)) {
-            *reinterpret_cast<YS *>(ybase + L.ya) = static_cast<YS>(f.mj);
-            L.ya += static_cast<uint32_t>(sizeof(YS));
-        }
-    } else if ((f.o == 7) & (L.ya < yend)) {
-        st_cell<SC, CT, SMEM>(base, L.ya, f.mj);
-        L.ya += q.row;
-    }
-    CT i2;
-    if constexpr (kRawI<POW2, AR>) i2 = L.i + static_cast<CT>(q.two);
-    else i2 = wrap<CT, AR>(L.i + 2, mask);
-    L.i = taken ? f.jw : (stay ? L.i : i2);
-}
 
 
 __device__ __forceinline__ uint32_t sel32(bool c, uint32_t a, uint32_t b)
@@ -736,7 +688,8 @@ __device__ __forceinline__ CT selw(bool c, CT a, CT b)
 // adds 2 (one conditional subtract of n, and i+2 wrapping through 2^w lands
 // on 0 or 1, its own residue), a taken branch reuses j mod n, which the
 // M[j] access computes anyway.  COUNT selects the move-counting form of
-// rasp_step_free, else the explicit form of rasp_step_free_t.
+// rasp_step_free (used by the epoch kernel), else the explicit form
+// (active &= !fixed; tlast = t while live).
 template <class SC, class CT, Arith AR, bool SMEM, bool COUNT, bool YG = false, class YS = SC>
 __device__ __forceinline__ void rasp_step_inc(LaneState<CT> &L, uint32_t &im, uint32_t &ib, char *base,
                                               uint32_t lm, uint32_t uend, uint32_t yend, const Geo &g,
@@ -838,9 +791,8 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     // warp-wide row moves (stmatrix/ldmatrix); BIG tiles keep per-lane moves
     // with 32 loads in flight (measured faster for their few resident warps)
     constexpr bool MX = SMEM && kMx<SC> && !BIG;
-    // ungated steps with move counting (every lane's budget covers the epoch;
-    // issue-bound shared-memory tiles -- big tiles keep the explicit form)
-    constexpr bool kCount = !BUDGET && AR != Arith::W1 && (!BIG || !POW2);
+    // ungated steps with move counting (every lane's budget covers the epoch)
+    constexpr bool kCount = !BUDGET && AR != Arith::W1;
     // ungated steps with carried residues (n not a power of two)
     constexpr bool kInc = !BUDGET && AR != Arith::W1 && !POW2 && SMEM;
     constexpr uint32_t kUnroll = RASP_UNROLL;
@@ -974,8 +926,6 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                     rasp_step_inc<SC, CT, AR, SMEM, kCount, BIG, S>(L, im, ib, tb, lm, uend, yend, g, q, t, ybase);
                     live = __any_sync(kFull, L.active);
                 }
-                if constexpr (!kCount)
-                    if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
             } else if constexpr (kCount) {
                 for (; live && t + UN <= K; t += UN) {
 #pragma unroll
@@ -987,29 +937,16 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                     rasp_step_free<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, ybase);
                     live = __any_sync(kFull, L.active);
                 }
-            } else {
-                if constexpr (!BUDGET && AR != Arith::W1) {
-                    for (; live && t + UN <= K; t += UN) {
-#pragma unroll
-                        for (uint32_t r = 0; r < UN; ++r)
-                            rasp_step_free_t<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + r, ybase);
-                        live = __any_sync(kFull, L.active);
-                    }
-                    for (; live && t < K; ++t) {
-                        rasp_step_free_t<SC, CT, POW2, AR, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, ybase);
-                        live = __any_sync(kFull, L.active);
-                    }
-                } else {
-                    for (; live && t + 2 <= K; t += 2) {
-                        rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
-                        rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, true, ybase);
-                        live = __any_sync(kFull, L.active);
-                    }
-                    if (live && t < K) {
-                        rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
-                        ++t;
-                        live = __any_sync(kFull, L.active);
-                    }
+            } else {   // per-lane budgets (mid-run inputs) or w = 1: the gated step
+                for (; live && t + 2 <= K; t += 2) {
+                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
+                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t + 1, true, ybase);
+                    live = __any_sync(kFull, L.active);
+                }
+                if (live && t < K) {
+                    rasp_step<SC, CT, POW2, AR, BUDGET, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, t, true, ybase);
+                    ++t;
+                    live = __any_sync(kFull, L.active);
                 }
                 if (live) rasp_step<SC, CT, POW2, AR, true, SMEM, BIG, S>(L, tb, lm, uend, yend, g, q, K, false, ybase);
             }
