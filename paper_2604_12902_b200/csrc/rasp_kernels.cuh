@@ -63,6 +63,9 @@ constexpr int kMaxEpochs = 1024;
 #ifndef RASP_UNROLL
 #define RASP_UNROLL 8
 #endif
+#ifndef RASP_UNROLL_BIG
+#define RASP_UNROLL_BIG 16
+#endif
 
 // Device-side epoch schedule (workspace).  Epoch e reads its length K[e] and
 // start offset covered[e]; the last block of epoch e writes K[e+1] from the
@@ -795,7 +798,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     constexpr bool kCount = !BUDGET && AR != Arith::W1;
     // ungated steps with carried residues (n not a power of two)
     constexpr bool kInc = !BUDGET && AR != Arith::W1 && !POW2 && SMEM;
-    constexpr uint32_t kUnroll = RASP_UNROLL;
+    constexpr uint32_t kUnroll = BIG ? RASP_UNROLL_BIG : RASP_UNROLL;
     const uint32_t tile0 = SMEM ? static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes : 0u;
     const bool vecM = mx_vec_ok<S, SC>(A.first ? A.in.M : A.out.M, n) && mx_vec_ok<S, SC>(A.out.M, n);
     char *ybase = nullptr;
