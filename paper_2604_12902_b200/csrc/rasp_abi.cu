@@ -84,6 +84,10 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.tile_rows = pl.tile_rows;
     a.stable_q8 = 128;                       // 0.5 (measured best on C2 and C5): tuning knob RASP_STABLE_Q8
     if (const char *e = std::getenv("RASP_STABLE_Q8")) a.stable_q8 = uint32_t(std::strtoul(e, nullptr, 10));
+    a.stable_hi_q8 = 243;                    // 0.95: tuning knob RASP_STABLE_HI_Q8
+    if (const char *e = std::getenv("RASP_STABLE_HI_Q8")) a.stable_hi_q8 = uint32_t(std::strtoul(e, nullptr, 10));
+    a.jump = 16;                             // tuning knob RASP_JUMP
+    if (const char *e = std::getenv("RASP_JUMP")) a.jump = uint32_t(std::strtoul(e, nullptr, 10));
     a.pf_dist = 1;                           // tuning knob RASP_PREFETCH (0 disables)
     if (const char *e = std::getenv("RASP_PREFETCH")) a.pf_dist = uint32_t(std::strtoul(e, nullptr, 10));
     cudaStream_t st = static_cast<cudaStream_t>(stream);

@@ -96,6 +96,8 @@ struct EpochArgs {
     uint32_t tile_rows;            // n + ell + 1 (+ s output rows unless BIG)
     uint32_t stable_q8;            // survival ratio (x256) at which the rest runs as one epoch
     uint32_t pf_dist;              // L2 prefetch distance in rounds of resident warps (0: off)
+    uint32_t jump;                 // longest "rest of the budget" epoch, in units of the previous one
+    uint32_t stable_hi_q8;         // survival ratio (x256) at which the rest runs as one epoch regardless
 };
 
 template <class CT, Arith AR>
@@ -1046,9 +1048,17 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const int64_t left = A.tau_max - cov;
             uint32_t kn = 0;
             if (cout > 0 && left > 0 && ntiles > 0) {
-                // once at least stable_q8/256 of the live set survives an epoch
-                // the rest runs as one epoch; otherwise keep compacting at 2x length
-                const bool stable = 256ull * cout >= static_cast<uint64_t>(A.stable_q8) * count;
+                // the rest of the budget runs as one epoch once the live set has
+                // stopped halting: at least stable_q8/256 of it survived this
+                // epoch and the rest is at most `jump` times this epoch, or
+                // stable_hi_q8/256 of it survived (a long budget jumped to while
+                // machines still halt leaves their lanes idle for all of it);
+                // otherwise keep compacting at 2x length
+                const uint64_t surv = 256ull * cout;
+                const bool stable =
+                    (surv >= static_cast<uint64_t>(A.stable_q8) * count &&
+                     static_cast<uint64_t>(left) <= static_cast<uint64_t>(A.jump) * (K > 0 ? K : 1u)) ||
+                    surv >= static_cast<uint64_t>(A.stable_hi_q8) * count;
                 const uint64_t want = stable ? static_cast<uint64_t>(left)
                                              : 2ull * (K > 0 ? K : 1u);
                 kn = static_cast<uint32_t>(min(min(want, static_cast<uint64_t>(left)),
