@@ -126,19 +126,27 @@ class Engine:
         s = stream if stream is not None else torch.cuda.current_stream(self.device)
         return s.cuda_stream
 
-    def workspace(self, d: int) -> torch.Tensor:
+    def workspace_bytes(self, d: int) -> int:
         with torch.cuda.device(self.device):
             need = self.lib.rasp_workspace_bytes(ctypes.byref(self._p), d)
         if need == 0 and d:
             raise NativeError("rasp_workspace_bytes failed")
+        return int(need)
+
+    def workspace(self, d: int) -> torch.Tensor:
+        """The engine's own workspace (runs on one stream at a time share it)."""
+        need = self.workspace_bytes(d)
         if self._ws is None or self._ws.numel() < need:
             self._ws = torch.empty(max(need, 256), dtype=torch.uint8, device=self.device)
         return self._ws
 
     def run(self, batch: DeviceBatch, tau_max: int, epoch: int = 64,
-            out: DeviceBatch | None = None, fresh: bool = False, stream=None) -> DeviceBatch:
+            out: DeviceBatch | None = None, fresh: bool = False, stream=None,
+            workspace: torch.Tensor | None = None) -> DeviceBatch:
         """Phi to fixed point or tau_max for every RUNNING machine (rasp_run).
-        In place unless `out` is given.  Asynchronous on `stream`."""
+        In place unless `out` is given.  Asynchronous on `stream`.  Runs that
+        may overlap on different streams need their own `workspace`
+        (workspace_bytes(d) bytes of device memory)."""
         if tau_max < 0:
             raise ValueError(f"tau_max must be >= 0, got {tau_max}")
         if epoch < 1:
@@ -148,7 +156,12 @@ class Engine:
             raise ValueError("out batch must match the input batch's size and word width")
         if batch.d == 0:
             return dst
-        ws = self.workspace(batch.d)
+        if workspace is not None:
+            if workspace.numel() < self.workspace_bytes(batch.d):
+                raise ValueError("workspace too small for this batch")
+            ws = workspace
+        else:
+            ws = self.workspace(batch.d)
         bi, bo = batch.c_struct(), dst.c_struct()
         with torch.cuda.device(self.device):
             rc = self.lib.rasp_run(ctypes.byref(self._p), ctypes.byref(bi), ctypes.byref(bo),

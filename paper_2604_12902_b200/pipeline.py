@@ -20,7 +20,7 @@ from .machine import MachineParams
 class HostPipeline:
     def __init__(self, params: MachineParams, d: int, device=None, chunks: int = 8,
                  engine: Engine | None = None, word_bytes: int | None = None, small_groups: int = 4,
-                 ramp: bool = True):
+                 ramp: bool = True, run_streams: int = 3):
         self.params = params
         self.d = d
         self.device = torch.device(device) if device is not None else torch.device("cuda")
@@ -44,7 +44,11 @@ class HostPipeline:
         self.host_out["steps"] = torch.empty(d, dtype=torch.int64, pin_memory=True)
         self.host_out["tau_h"] = torch.empty(d, dtype=torch.int64, pin_memory=True)
         self.s_in = torch.cuda.Stream(self.device)
-        self.s_run = torch.cuda.Stream(self.device)
+        # chunk runs alternate between run streams, so one chunk's long tail
+        # (its last machines in a long epoch) overlaps the next chunk's run;
+        # each stream has its own workspace
+        self.s_runs = [torch.cuda.Stream(self.device) for _ in range(max(1, run_streams))]
+        self.s_run = self.s_runs[0]
         self.s_out = torch.cuda.Stream(self.device)
         self.h2d_bytes = 0
         self.d2h_bytes = sum(t.numel() * t.element_size() for t in self.host_out.values())
@@ -52,8 +56,9 @@ class HostPipeline:
         # few large copies -- each copy costs ~10 us of PCIe time, and 8 fields
         # x chunks of them cost more than the overlap wins (scripts/pcie_split.py)
         self.small_groups = max(1, min(small_groups, len(self.bounds)))
-        # one workspace per in-flight run (runs are serial on s_run, so one suffices)
-        self.engine.workspace(max((b - a for a, b in self.bounds), default=0))
+        # one workspace per run stream
+        wsb = self.engine.workspace_bytes(max((b - a for a, b in self.bounds), default=0))
+        self.ws = [torch.empty(max(wsb, 256), dtype=torch.uint8, device=self.device) for _ in self.s_runs]
 
     def pinned_inputs(self, arrays: dict) -> dict:
         """Copy host c0 arrays (numpy) into pinned tensors once."""
@@ -79,7 +84,7 @@ class HostPipeline:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(main)
-        for s in (self.s_in, self.s_run, self.s_out):
+        for s in (self.s_in, *self.s_runs, self.s_out):
             s.wait_event(e0)
         for c, (a, b) in enumerate(self.bounds):
             with torch.cuda.stream(self.s_in):
@@ -87,11 +92,12 @@ class HostPipeline:
                     getattr(self.dev, k)[a:b].copy_(pinned[k][a:b], non_blocking=True)
                 ev_in = torch.cuda.Event()
                 ev_in.record(self.s_in)
-            self.s_run.wait_event(ev_in)
+            sr, ws = self.s_runs[c % len(self.s_runs)], self.ws[c % len(self.s_runs)]
+            sr.wait_event(ev_in)
             # fresh c0: status/steps/tau_h are outputs only, never read
-            self.engine.run(self._view(self.dev, a, b), tau_max, epoch, fresh=True, stream=self.s_run)
+            self.engine.run(self._view(self.dev, a, b), tau_max, epoch, fresh=True, stream=sr, workspace=ws)
             ev_run = torch.cuda.Event()
-            ev_run.record(self.s_run)
+            ev_run.record(sr)
             self.s_out.wait_event(ev_run)
             self._copy_out(c, a, b)
         main.wait_stream(self.s_out)
@@ -127,7 +133,7 @@ class HostPipeline:
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(main)
-        for s in (self.s_in, self.s_run, self.s_out):
+        for s in (self.s_in, *self.s_runs, self.s_out):
             s.wait_event(e0)
         P, X = self._stage["programs"], self._stage["inputs"]
         for c, (a, b) in enumerate(self.bounds):
@@ -137,12 +143,13 @@ class HostPipeline:
                     X[a:b].copy_(pinned["inputs"][a:b], non_blocking=True)
                 ev_in = torch.cuda.Event()
                 ev_in.record(self.s_in)
-            self.s_run.wait_event(ev_in)
+            sr, ws = self.s_runs[c % len(self.s_runs)], self.ws[c % len(self.s_runs)]
+            sr.wait_event(ev_in)
             view = self._view(self.dev, a, b)
-            self.engine.init_c0(P[a:b], X[a:b], view, stream=self.s_run)
-            self.engine.run(view, tau_max, epoch, fresh=True, stream=self.s_run)
+            self.engine.init_c0(P[a:b], X[a:b], view, stream=sr)
+            self.engine.run(view, tau_max, epoch, fresh=True, stream=sr, workspace=ws)
             ev_run = torch.cuda.Event()
-            ev_run.record(self.s_run)
+            ev_run.record(sr)
             self.s_out.wait_event(ev_run)
             self._copy_out(c, a, b)
         main.wait_stream(self.s_out)
