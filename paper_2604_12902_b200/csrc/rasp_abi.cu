@@ -86,6 +86,8 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     if (const char *e = std::getenv("RASP_STABLE_Q8")) a.stable_q8 = uint32_t(std::strtoul(e, nullptr, 10));
     a.stable_hi_q8 = 243;                    // 0.95: tuning knob RASP_STABLE_HI_Q8
     if (const char *e = std::getenv("RASP_STABLE_HI_Q8")) a.stable_hi_q8 = uint32_t(std::strtoul(e, nullptr, 10));
+    a.growth = 2;                            // tuning knob RASP_GROWTH (>= 2: the host plans for doubling)
+    if (const char *e = std::getenv("RASP_GROWTH")) a.growth = std::max<uint32_t>(2, uint32_t(std::strtoul(e, nullptr, 10)));
     a.jump = 16;                             // tuning knob RASP_JUMP
     if (const char *e = std::getenv("RASP_JUMP")) a.jump = uint32_t(std::strtoul(e, nullptr, 10));
     a.pf_dist = 1;                           // tuning knob RASP_PREFETCH (0 disables)

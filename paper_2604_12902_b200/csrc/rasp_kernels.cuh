@@ -97,6 +97,7 @@ struct EpochArgs {
     uint32_t stable_q8;            // survival ratio (x256) at which the rest runs as one epoch
     uint32_t pf_dist;              // L2 prefetch distance in rounds of resident warps (0: off)
     uint32_t jump;                 // longest "rest of the budget" epoch, in units of the previous one
+    uint32_t growth;               // next epoch length while machines still halt, x the last one
     uint32_t stable_hi_q8;         // survival ratio (x256) at which the rest runs as one epoch regardless
 };
 
@@ -1060,7 +1061,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                      static_cast<uint64_t>(left) <= static_cast<uint64_t>(A.jump) * (K > 0 ? K : 1u)) ||
                     surv >= static_cast<uint64_t>(A.stable_hi_q8) * count;
                 const uint64_t want = stable ? static_cast<uint64_t>(left)
-                                             : 2ull * (K > 0 ? K : 1u);
+                                             : static_cast<uint64_t>(A.growth) * (K > 0 ? K : 1u);
                 kn = static_cast<uint32_t>(min(min(want, static_cast<uint64_t>(left)),
                                                static_cast<uint64_t>(A.kmax)));
             }
