@@ -45,7 +45,7 @@ inline uint32_t max_epoch_len()
     }();
     return v;
 }
-constexpr int kWarpsPerBlockMax = 4;
+constexpr int kWarpsPerBlockMax = RASP_BLOCK_WARPS;
 constexpr size_t kBigTile = 16 * 1024;  // tiles above this use the one-warp, many-register kernel
 constexpr size_t kGlobalTileBudget = size_t(1) << 30;  // bytes of HBM tiles for huge n
 

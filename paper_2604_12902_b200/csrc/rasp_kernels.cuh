@@ -66,6 +66,18 @@ constexpr int kMaxEpochs = 1024;
 #ifndef RASP_UNROLL_BIG
 #define RASP_UNROLL_BIG 16
 #endif
+// Launch shape of the shared-memory epoch kernels: at most RASP_BLOCK_WARPS
+// warps per block, RASP_MIN_BLOCKS blocks resident per SM (caps registers).
+#ifndef RASP_BLOCK_WARPS
+#define RASP_BLOCK_WARPS 4
+#endif
+#ifndef RASP_MIN_BLOCKS
+#define RASP_MIN_BLOCKS 10
+#endif
+// Matrix-op row moves in flight per lane (16 B each) when loading a tile.
+#ifndef RASP_MX_BATCH
+#define RASP_MX_BATCH 4
+#endif
 
 // Device-side epoch schedule (workspace).  Epoch e reads its length K[e] and
 // start offset covered[e]; the last block of epoch e writes K[e+1] from the
@@ -761,12 +773,12 @@ __device__ __forceinline__ void rasp_step_inc(LaneState<CT> &L, uint32_t &im, ui
 }
 
 template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM, bool BIG = false>
-__global__ void __launch_bounds__(BIG ? 32 : 128, BIG ? 8 : (SMEM ? 10 : 1))
+__global__ void __launch_bounds__(BIG ? 32 : 32 * RASP_BLOCK_WARPS, BIG ? 8 : (SMEM ? RASP_MIN_BLOCKS : 1))
 epoch_kernel(const EpochArgs A, SC *gtiles)
 {
     constexpr uint32_t LB = BIG ? 32 : 8;   // row-load batch (per-lane path)
     // matrix-op batch (16 B per lane each): wide only for native-width rows
-    constexpr uint32_t MB = 4;
+    constexpr uint32_t MB = RASP_MX_BATCH;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr uint32_t ROW = 32 * sizeof(SC);
     const uint32_t lane = threadIdx.x & 31;
