@@ -399,13 +399,15 @@ __device__ __forceinline__ void mx_store(S *__restrict__ row, bool valid, bool v
 }
 
 
-// Bulk L2 prefetch of [p, p + bytes) (rounded out to 16-byte granules).
+// L2 prefetch of [p, p + bytes): one per-lane prefetch per 128-byte line.
+// (The bulk form, cp.async.bulk.prefetch, takes a warp-uniform address: with
+// every lane prefetching its own machine's row ptxas runs it as a 32-step
+// waterfall loop per call -- ~8% of the first epoch's instructions on C2.)
 __device__ __forceinline__ void prefetch_l2(const void *p, uint32_t bytes)
 {
-    const uintptr_t a = reinterpret_cast<uintptr_t>(p);
-    const uintptr_t lo = a & ~uintptr_t(15), hi = (a + bytes + 15) & ~uintptr_t(15);
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(lo), "r"(static_cast<uint32_t>(hi - lo))
-                 : "memory");
+    const uintptr_t end = reinterpret_cast<uintptr_t>(p) + bytes;
+    for (uintptr_t a = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(127); a < end; a += 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
 }
 
 
