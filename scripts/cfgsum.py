@@ -1,6 +1,6 @@
 import json,sys
 tag=sys.argv[1]
-for c in ("c1","c2","c3","c4","c5","paper"):
+for c in ("c1","c2","c3","c4","c5","paper","paper6"):
     try:
         d=json.loads(open(f'gpurun_out/{tag}_bench_{c}.log').read().strip().splitlines()[-1])
     except Exception as e:

@@ -49,6 +49,9 @@ for i, r in enumerate(rows[2:]):
         v = d.get(key, "")
         if key.startswith("dram__bytes") and v:
             v = f"{v} {u.get(key, '')}"
+        if key == "gpu__time_duration.sum" and v:   # ncu picks the unit per launch
+            scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}.get(u.get(key, ""), 1.0)
+            v = f"{float(v.replace(',', '')) * scale:.3f}"
         vals.append(v)
     lines.append(f"| {i} | `{kname}` | " + " | ".join(vals) + " |")
 
