@@ -778,6 +778,12 @@ template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SM
 __global__ void __launch_bounds__(BIG ? 32 : 32 * RASP_BLOCK_WARPS, BIG ? 8 : (SMEM ? RASP_MIN_BLOCKS : 1))
 epoch_kernel(const EpochArgs A, SC *gtiles)
 {
+    // Programmatic dependent launch: epochs after the first are launched while
+    // the previous one drains; wait for it (complete, memory visible) before
+    // touching anything, then let the next epoch's blocks queue behind this one.
+    // Both are no-ops for a launch without the PDL attribute.
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     constexpr uint32_t LB = BIG ? 32 : 8;   // row-load batch (per-lane path)
     // matrix-op batch (16 B per lane each): wide only for native-width rows
     constexpr uint32_t MB = RASP_MX_BATCH;
