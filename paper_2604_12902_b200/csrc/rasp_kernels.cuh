@@ -780,10 +780,10 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
 {
     // Programmatic dependent launch: epochs after the first are launched while
     // the previous one drains; wait for it (complete, memory visible) before
-    // touching anything, then let the next epoch's blocks queue behind this one.
-    // Both are no-ops for a launch without the PDL attribute.
+    // touching anything (a no-op for a launch without the PDL attribute).  No
+    // early launch_dependents: the next epoch's blocks would sit on the SMs
+    // through this epoch's tail, where runs on other streams could use them.
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     constexpr uint32_t LB = BIG ? 32 : 8;   // row-load batch (per-lane path)
     // matrix-op batch (16 B per lane each): wide only for native-width rows
     constexpr uint32_t MB = RASP_MX_BATCH;

@@ -331,6 +331,46 @@ def test_cuda_graph_replay_matches_eager(pkg):
         assert torch.equal(hist, href)
 
 
+def test_cuda_graph_replays_follow_each_batch_schedule(pkg):
+    """One captured launch sequence serves batches whose device-side schedules
+    differ: a replay on a batch that needs every planned epoch after one whose
+    machines all halt at t = 0 (schedule over after the first epoch) still
+    matches eager runs, in either order."""
+    import torch
+    P, H = pkg
+    from paper_2604_12902_b200.engine import DeviceBatch
+    from paper_2604_12902_b200.workload import synthetic_c0
+    p = P.MachineParams(w=16, n=64, ell=8, s=8, mu=1)
+    dev = torch.device("cuda:0")
+    long_c0 = synthetic_c0(20_000, p, seed=4)
+    quick_c0 = {k: v.copy() for k, v in long_c0.items()}
+    quick_c0["M"][:] = 0          # opcode 0 everywhere: every machine is fixed at t = 0
+    eng = H.get_engine(p, dev)
+    refs = {}
+    for name, c0 in (("long", long_c0), ("quick", quick_c0)):
+        b = DeviceBatch.from_arrays(c0, p, dev)
+        r = DeviceBatch.empty(b.d, p, dev, fresh=False)
+        eng.run(b, 1024, 32, out=r, fresh=True)
+        refs[name] = (b, r)
+    src = DeviceBatch.from_arrays(long_c0, p, dev)
+    dst = DeviceBatch.empty(src.d, p, dev, fresh=False)
+    cap = torch.cuda.Stream(dev)
+    cap.wait_stream(torch.cuda.current_stream(dev))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cap):
+        eng.run(src, 1024, 32, out=dst, fresh=True, stream=cap)
+    for name in ("quick", "long", "quick", "long"):
+        b, r = refs[name]
+        for k in ("iw", "ac", "M", "u", "y"):
+            getattr(src, k).copy_(getattr(b, k))
+        for k in ("iw", "M", "steps", "status"):
+            getattr(dst, k).zero_()
+        g.replay()
+        torch.cuda.synchronize()
+        for k in ("iw", "ac", "M", "u", "y", "status", "steps", "tau_h"):
+            assert torch.equal(getattr(dst, k), getattr(r, k)), (name, k)
+
+
 _LONG_BUDGET = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
