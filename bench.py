@@ -293,7 +293,7 @@ def bench_enumeration(args, world, rank, dev, desc):
         dist.destroy_process_group()
 
 
-DEFAULT_EPOCH = {"c1": 64, "c2": 48, "c3": 48, "c5": 384, "paper": 32, "paper6": 32}
+DEFAULT_EPOCH = {"c1": 64, "c2": 48, "c3": 48, "c5": 320, "paper": 32, "paper6": 32}
 
 
 def main():

@@ -1080,8 +1080,14 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                     (surv >= static_cast<uint64_t>(A.stable_q8) * count &&
                      static_cast<uint64_t>(left) <= static_cast<uint64_t>(A.jump) * (K > 0 ? K : 1u)) ||
                     surv >= static_cast<uint64_t>(A.stable_hi_q8) * count;
-                const uint64_t want = stable ? static_cast<uint64_t>(left)
-                                             : static_cast<uint64_t>(A.growth) * (K > 0 ? K : 1u);
+                uint64_t want = stable ? static_cast<uint64_t>(left)
+                                       : static_cast<uint64_t>(A.growth) * (K > 0 ? K : 1u);
+                // never leave a sliver of the budget (under a quarter of this
+                // epoch) for one more epoch: it would reload every survivor
+                // for a few steps (C5 at first epoch 336: 336, 672, 16)
+                if (static_cast<uint64_t>(left) > want &&
+                    static_cast<uint64_t>(left) - want < (want >> 2))
+                    want = static_cast<uint64_t>(left);
                 kn = static_cast<uint32_t>(min(min(want, static_cast<uint64_t>(left)),
                                                static_cast<uint64_t>(A.kmax)));
             }
