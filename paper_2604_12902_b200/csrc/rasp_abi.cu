@@ -152,9 +152,14 @@ int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t cou
     const size_t smem = size_t(8) * (ep->n + 3) * 64;
     const bool pow2 = (ep->n & (ep->n - 1)) == 0;
     auto kern = pow2 ? rasp::enum_kernel<true, rasp::Arith::NARROW> : rasp::enum_kernel<false, rasp::Arith::NARROW>;
-    RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (smem > size_t(dv.smem_optin)) return RASP_ECAPACITY;
     int per_sm = 0;
-    RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    {
+        std::lock_guard<std::mutex> lock(launch_mutex());
+        rc = raise_smem_limit_locked(reinterpret_cast<const void *>(kern), dv);
+        if (rc) return rc;
+        RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, smem));
+    }
     if (per_sm < 1) return RASP_ECAPACITY;
     // one resident wave of blocks; every warp loops over whole programs
     const uint64_t grid = std::min<uint64_t>((count + 7) / 8, uint64_t(per_sm) * dv.nsm);

@@ -11,6 +11,9 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 namespace rasp {
 namespace host {
@@ -76,6 +79,63 @@ inline int device_info(Device &dv)
         cache = d;
     }
     dv = cache;
+    return RASP_OK;
+}
+
+// Launch shape of a kernel for one dynamic shared-memory size per unit
+// (tile or slot group): units per block and resident blocks per SM, chosen to
+// maximise resident units per SM.  Process-wide cache guarded by a mutex; the
+// kernel's MaxDynamicSharedMemorySize attribute is raised once per (kernel,
+// device) to the opt-in maximum and never lowered, so concurrent callers on
+// other threads never see a limit below their launch (occupancy queries take
+// each candidate size as an argument).
+struct LaunchShape { int units = 0; int per_sm = 0; };
+
+inline std::mutex &launch_mutex()
+{
+    static std::mutex mu;
+    return mu;
+}
+
+// Raise a kernel's dynamic shared-memory limit to the device's opt-in maximum,
+// once per (kernel, device); the caller holds launch_mutex().
+inline int raise_smem_limit_locked(const void *kern, const Device &dv)
+{
+    static std::map<std::pair<const void *, int>, bool> raised;
+    if (!raised[std::make_pair(kern, dv.id)]) {
+        RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dv.smem_optin));
+        raised[std::make_pair(kern, dv.id)] = true;
+    }
+    return RASP_OK;
+}
+
+inline int launch_shape(const void *kern, const Device &dv, size_t unit_bytes, size_t fixed_bytes, int max_units,
+                        LaunchShape &out)
+{
+    static std::map<std::tuple<const void *, int, size_t, size_t, int>, LaunchShape> shapes;
+    std::lock_guard<std::mutex> lock(launch_mutex());
+    const auto key = std::make_tuple(kern, dv.id, unit_bytes, fixed_bytes, max_units);
+    const auto it = shapes.find(key);
+    if (it != shapes.end()) {
+        out = it->second;
+        return RASP_OK;
+    }
+    const int rc = raise_smem_limit_locked(kern, dv);
+    if (rc) return rc;
+    LaunchShape best;
+    for (int u = max_units; u >= 1; --u) {
+        const size_t smem = fixed_bytes + unit_bytes * size_t(u);
+        if (smem > size_t(dv.smem_optin)) continue;
+        int per_sm = 0;
+        RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * u, smem));
+        if (per_sm * u > best.per_sm * best.units) {
+            best.units = u;
+            best.per_sm = per_sm;
+        }
+    }
+    if (best.units == 0) return RASP_ECAPACITY;
+    shapes[key] = best;
+    out = best;
     return RASP_OK;
 }
 
@@ -164,37 +224,17 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
     auto kern = rasp::epoch_kernel<S, SC, CT, POW2, AR, BUDGET, SMEM, BIG>;
     if (SMEM) {
         // warps per block chosen to maximise resident warps per SM (ties: more
-        // warps per block); attribute + occupancy queried once per
-        // (instantiation, device, tile size)
-        struct Cached { int dev = -1; size_t tile = 0; int wpb = 0; int per_sm = 0; };
-        static thread_local Cached c;
-        if (c.dev != dv.id || c.tile != pl.tile_bytes) {
-            int best_w = 0, best_ps = 0;
-            for (int wpb = BIG ? 1 : kWarpsPerBlockMax; wpb >= 1; --wpb) {
-                const size_t smem = pl.tile_bytes * size_t(wpb);
-                if (smem > size_t(dv.smem_optin)) continue;
-                RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-                int per_sm = 0;
-                RASP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * wpb, smem));
-                if (per_sm * wpb > best_ps * best_w) {
-                    best_w = wpb;
-                    best_ps = per_sm;
-                }
-            }
-            if (best_w == 0) return RASP_ECAPACITY;
-            RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           int(pl.tile_bytes * size_t(best_w))));
-            c.dev = dv.id;
-            c.tile = pl.tile_bytes;
-            c.wpb = best_w;
-            c.per_sm = best_ps;
-        }
-        pl.warps_per_block = c.wpb;
-        pl.dyn_smem = pl.tile_bytes * size_t(c.wpb);
-        pl.blocks = c.per_sm * dv.nsm;
+        // warps per block)
+        LaunchShape sh;
+        const int rc = launch_shape(reinterpret_cast<const void *>(kern), dv, pl.tile_bytes, 0,
+                                    BIG ? 1 : kWarpsPerBlockMax, sh);
+        if (rc) return rc;
+        pl.warps_per_block = sh.units;
+        pl.dyn_smem = pl.tile_bytes * size_t(sh.units);
+        pl.blocks = sh.per_sm * dv.nsm;
         if (std::getenv("RASP_DEBUG"))   // plan of this launch sequence (tuning aid)
             std::fprintf(stderr, "rasp: tile %zu B (%u rows), %d warps/block, %d blocks/SM, big %d\n",
-                         pl.tile_bytes, pl.tile_rows, c.wpb, c.per_sm, int(BIG));
+                         pl.tile_bytes, pl.tile_rows, sh.units, sh.per_sm, int(BIG));
     }
     const int threads = 32 * pl.warps_per_block;
     const uint64_t tiles = (d + 31) / 32;
@@ -226,7 +266,15 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
         else (void)cudaGetLastError();   // e.g. legacy stream during a global capture
     }
     for (int e = 0;; ++e) {
-        if (e >= kMaxEpochs) return RASP_ECAPACITY;
+        if (e >= kMaxEpochs) {
+            // the schedule slots are used up: fine if the last epoch left no
+            // survivors (its K[e+1] is never written), a capacity error if not
+            uint32_t left = 0;
+            RASP_CUDA(cudaMemcpyAsync(&left, &ws.sched->count[kMaxEpochs - 1], sizeof left, cudaMemcpyDeviceToHost, st));
+            RASP_CUDA(cudaStreamSynchronize(st));
+            if (left == 0) break;
+            return RASP_ECAPACITY;
+        }
         if (e >= planned && covers) break;   // fully asynchronous in the common case
         if (e >= planned) {
             // long budgets: ask the device whether another epoch is needed

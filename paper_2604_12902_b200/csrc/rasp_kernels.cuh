@@ -111,6 +111,7 @@ struct EpochArgs {
     uint32_t jump;                 // longest "rest of the budget" epoch, in units of the previous one
     uint32_t growth;               // next epoch length while machines still halt, x the last one
     uint32_t stable_hi_q8;         // survival ratio (x256) at which the rest runs as one epoch regardless
+    unsigned long long *hist;      // int64[102] halting histogram accumulated by the run, or nullptr
 };
 
 template <class CT, Arith AR>
@@ -866,6 +867,9 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                           (m1 - m0) * ucols * sizeof(S), lane);
                 warp_copy(static_cast<S *>(dst.y) + m0 * ycols, static_cast<const S *>(A.in.y) + m0 * ycols,
                           (m1 - m0) * ycols * sizeof(S), lane);
+                // the owning lanes rewrite u[0], y[0] and y[k] of these rows at
+                // write-back: order the copies (any lane) before those stores
+                __syncwarp();
             }
             const uint32_t j = tix * 32 + lane;
             const bool valid = j < count;

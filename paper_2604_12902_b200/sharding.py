@@ -69,26 +69,28 @@ def reduce_histogram(hist: torch.Tensor, group=None) -> torch.Tensor:
     return hist
 
 
-def gather_to_root(t: torch.Tensor, d_total: int, world: int, rank: int, group=None):
+def gather_to_root(t: torch.Tensor, d_total: int, world: int, rank: int, group=None, sizes=None):
     """Gather contiguous shards of a per-machine tensor to rank 0.
 
-    Shards may differ in length by the partition; every rank pads to the
-    largest shard so one collective moves everything.  Returns the full
-    [d_total, ...] tensor on rank 0, None elsewhere."""
+    Shards may differ in length by the partition (`sizes`: machines per rank,
+    default shard_bounds(d_total, world, k)); every rank pads to the largest
+    shard so one collective moves everything.  Returns the full [d_total, ...]
+    tensor on rank 0, None elsewhere."""
     if not (dist.is_available() and dist.is_initialized()) or world == 1:
         return t
-    per = -(-d_total // world) if d_total else 0
-    pad = torch.zeros((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
-    pad[: t.shape[0]] = t
+    if sizes is None:
+        sizes = [hi - lo for lo, hi in (shard_bounds(d_total, world, k) for k in range(world))]
+    per = max(sizes) if sizes else 0
+    if t.shape[0] == per:
+        pad = t.contiguous()
+    else:
+        pad = torch.zeros((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
+        pad[: t.shape[0]] = t
     parts = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
     dist.gather(pad, parts, dst=0, group=group)
     if rank != 0:
         return None
-    out = []
-    for k in range(world):
-        lo, hi = shard_bounds(d_total, world, k)
-        out.append(parts[k][: hi - lo])
-    return torch.cat(out, 0)
+    return torch.cat([parts[k][: sizes[k]] for k in range(world)], 0)
 
 
 def collect(status: torch.Tensor, steps: torch.Tensor, tau_h: torch.Tensor, y: torch.Tensor,

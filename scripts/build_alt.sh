@@ -1,6 +1,6 @@
 #!/bin/bash
 # /tmp/buildalt.sh <name> <extra nvcc flags...>
-cd /root/repo
+cd "$(dirname "$0")/.."
 NAME=$1; shift
 mkdir -p build/$NAME
 pids=()

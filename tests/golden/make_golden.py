@@ -254,7 +254,54 @@ def fam_gen():
     f.save()
 
 
-ALL = (fam_kat, fam_edge, fam_corpus, fam_hyp, fam_bb, fam_paper, fam_paper100, fam_gen)
+def fam_packer():
+    """Inputs and outputs of the reference's packer init_config (m:289-309)
+    for the programs the bb/paper/paper100 families run: the lowered program
+    words (zero-padded to the longest program, `plen` = each length), the
+    sampled input words (zero-padded, `xlen` = each count) and the c0 that
+    init_config returned.  The device packer rasp_init_c0 is pinned to it."""
+    from raspvisor.sampler import sample_inputs, sample_program
+    p32 = RM.MachineParams(w=32, n=250, ell=10, s=2, mu=10)
+    data = {}
+    sets = {}
+    progs = []
+    for k in (1, 2, 3):
+        with open(os.path.join(REF_FIX, f"bb{k}.arr"), encoding="utf-8") as fh:
+            prog, _ = lower(parse_source(fh.read()), p32)
+        progs.append((prog, ()))
+    sets["bb"] = progs
+    for name, length, count, seed in (("paper", 30, 64, 3), ("paper100", 100, 512, 5)):
+        progs = []
+        for k in range(count):   # the loop of build_workload (hypervisor.py:362-384)
+            ast = sample_program(length, seed, k, None)
+            inputs = sample_inputs(ast.n_in, p32.w, seed, k)
+            try:
+                prog, _ = lower(ast, p32)
+            except RM.CapacityError:
+                continue
+            progs.append((prog, tuple(inputs)))
+        sets[name] = progs
+    for name, progs in sets.items():
+        L = max(len(pr.words) for pr, _ in progs)
+        X = max(1, max(len(x) for _, x in progs))
+        P = np.zeros((len(progs), L), np.uint64)
+        Xa = np.zeros((len(progs), X), np.uint64)
+        for r, (pr, x) in enumerate(progs):
+            P[r, :len(pr.words)] = pr.words
+            Xa[r, :len(x)] = x
+        c0 = _arrays([RM.init_config(pr, x, p32) for pr, x in progs], p32)
+        data[f"{name}_prog"] = P
+        data[f"{name}_plen"] = np.array([len(pr.words) for pr, _ in progs], np.int64)
+        data[f"{name}_inp"] = Xa
+        data[f"{name}_xlen"] = np.array([len(x) for _, x in progs], np.int64)
+        for k, v in c0.items():
+            data[f"{name}_c0_{k}"] = v
+    path = os.path.join(HERE, "packer.npz")
+    np.savez_compressed(path, **data)
+    print(f"packer: {sorted(sets)} -> {os.path.relpath(path, REPO)} ({os.path.getsize(path) / 1024:.1f} KiB)")
+
+
+ALL = (fam_kat, fam_edge, fam_corpus, fam_hyp, fam_bb, fam_paper, fam_paper100, fam_gen, fam_packer)
 
 if __name__ == "__main__":
     H._warm_kernel()
