@@ -13,7 +13,7 @@ that config: rank 0 gathers every shard's verdicts and output tapes over
 NCCL (--gather on|off overrides); c1 and c5 are configs[0] and configs[4].
 
 One "step" = one full run of the batch from c0 (out-of-place, c0 is never
-modified) plus the on-device halting histogram.  Metric: machine-steps/s
+modified) with the halting histogram counted inside the run (rasp_run_hist).  Metric: machine-steps/s
 (sum of per-machine applied steps, hypervisor.py:153, over all ranks / max
 per-rank device time).
 
@@ -602,9 +602,8 @@ def bench_batch(args, world, rank, local_rank, dev):
     do_gather = world > 1 and args.gather == "on"
     sizes = [sum(m for _, m in rank_shards(args.config, world, r, args.shard_machines)) for r in range(world)]
 
-    def run_step(st):
-        eng.run(src, tau, args.epoch, out=dst, fresh=True, stream=st)
-        eng.histogram(dst, out=hist, stream=st)
+    def run_step(st):   # the run with its halting histogram counted in the epoch kernels
+        eng.run(src, tau, args.epoch, out=dst, fresh=True, stream=st, hist=hist)
 
     def collectives():
         """N > 1: halt counts all-reduced, verdicts + output tapes gathered to
@@ -613,8 +612,8 @@ def bench_batch(args, world, rank, local_rank, dev):
         dist.all_reduce(h)
         if gloo:
             hist.copy_(h)
-        if do_gather:
-            for t in (dst.status, dst.steps, dst.tau_h, dst.y):
+        if do_gather:   # output tapes travel as bytes (no uint16 collectives in NCCL or gloo)
+            for t in (dst.status, dst.steps, dst.tau_h, dst.y.view(torch.uint8)):
                 tt = t.cpu() if gloo else t
                 gather_to_root(tt, d_total, world, rank, sizes=sizes)
 
@@ -628,7 +627,7 @@ def bench_batch(args, world, rank, local_rank, dev):
     torch.cuda.synchronize()
     launches_per_step = lib.rasp_launch_count() - l0
 
-    # capture the per-rank step (rasp_run + histogram) in a CUDA graph and time
+    # capture the per-rank step (rasp_run_hist) in a CUDA graph and time
     # its replays -- the same kernels without host enqueue gaps; at N > 1 the
     # collectives follow the replay inside the timed region
     graph, graph_note = None, None
@@ -757,7 +756,7 @@ def bench_batch(args, world, rank, local_rank, dev):
         "run": {"machines_per_gpu": d, "shards_rank0": [k for k, _ in shards], "epoch": args.epoch,
                 "machine_steps": total_steps, "halted_frac": total_halted / d_total,
                 "l2": "flushed between steps (256 MB write, outside the events)",
-                "launch": ("CUDA graph replay of rasp_run + histogram" if graph is not None else
+                "launch": ("CUDA graph replay of rasp_run_hist (histogram fused)" if graph is not None else
                            "eager launches" + (f" ({graph_note})" if graph_note else ""))
                           + (f", then NCCL all-reduce(histogram)" + (" + gather(status, steps, tau_h, y) to rank 0"
                                                                       if do_gather else "") if world > 1 else ""),

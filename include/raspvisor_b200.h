@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define RASP_ABI_VERSION 2
+#define RASP_ABI_VERSION 3
 
 /* error codes */
 #define RASP_OK 0
@@ -97,6 +97,18 @@ size_t rasp_workspace_bytes(const rasp_params *p, uint64_t d);
 int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out,
              int64_t tau_max, int64_t epoch, uint32_t flags,
              void *workspace, size_t workspace_bytes, void *stream);
+
+/* rasp_run plus the halting histogram of the batch after the run, computed
+ * inside the epoch kernels (each verdict counted as it is written; machines
+ * entering with status != 0 counted as they stand): hist[0..99] = machines
+ * HALTED with tau_h = k, hist[100] = HALTED with tau_h >= 100, hist[101] =
+ * EXHAUSTED -- collect_histogram / HISTOGRAM_KEYS (hypervisor.py:326-352).
+ * `hist` is a device int64[102], zeroed by the call; NULL = plain rasp_run.
+ * Replaces rasp_run + rasp_histogram (one launch and a 9 B/machine re-read
+ * fewer). */
+int rasp_run_hist(const rasp_params *p, const rasp_batch *in, const rasp_batch *out,
+                  int64_t tau_max, int64_t epoch, uint32_t flags, int64_t *hist,
+                  void *workspace, size_t workspace_bytes, void *stream);
 
 /* Device packer of init_config (machine.py:289-309) for a whole batch:
  * M = program || 0, u = (0, inputs || 0), y = 0, i = a = 0, status = 0,

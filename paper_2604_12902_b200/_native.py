@@ -16,12 +16,12 @@ from .errors import NativeError
 LIB_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "_lib")
 # RASP_LIBRARY: load another build of the same library (A/B timing of kernel variants)
 LIB_PATH = os.environ.get("RASP_LIBRARY") or os.path.join(LIB_DIR, "libraspvisor_b200.so")
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 RASP_FRESH = 1
 
 # symbols declared by include/raspvisor_b200.h
-EXPORTS = ("rasp_workspace_bytes", "rasp_run", "rasp_histogram", "rasp_validate",
+EXPORTS = ("rasp_workspace_bytes", "rasp_run", "rasp_run_hist", "rasp_histogram", "rasp_validate",
            "rasp_error_string", "rasp_last_cuda_error", "rasp_abi_version",
            "rasp_launch_count", "rasp_enumerate", "rasp_init_c0", "rasp_generate",
            "rasp_pack", "rasp_unpack", "rasp_topk_workspace_bytes", "rasp_topk",
@@ -76,6 +76,8 @@ def load():
     lib.rasp_workspace_bytes.restype = SZ
     lib.rasp_run.argtypes = [pp, pb, pb, I64, I64, U32, P, SZ, P]
     lib.rasp_run.restype = ctypes.c_int
+    lib.rasp_run_hist.argtypes = [pp, pb, pb, I64, I64, U32, P, P, SZ, P]
+    lib.rasp_run_hist.restype = ctypes.c_int
     lib.rasp_histogram.argtypes = [P, P, U64, P, P]
     lib.rasp_histogram.restype = ctypes.c_int
     lib.rasp_validate.argtypes = [pp, pb, P, P]

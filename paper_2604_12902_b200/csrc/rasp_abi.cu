@@ -47,11 +47,19 @@ size_t rasp_workspace_bytes(const rasp_params *p, uint64_t d)
 int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, int64_t tau_max,
              int64_t epoch, uint32_t flags, void *workspace, size_t workspace_bytes, void *stream)
 {
+    return rasp_run_hist(p, in, out, tau_max, epoch, flags, nullptr, workspace, workspace_bytes, stream);
+}
+
+int rasp_run_hist(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, int64_t tau_max,
+                  int64_t epoch, uint32_t flags, int64_t *hist, void *workspace, size_t workspace_bytes,
+                  void *stream)
+{
     int rc = check_params(p);
     if (rc) return rc;
     if (!in || !out || tau_max < 0 || epoch < 1) return RASP_EPARAM;
     if (in->d != out->d) return RASP_EPARAM;
     const uint64_t d = in->d;
+    if (hist) RASP_CUDA(cudaMemsetAsync(hist, 0, sizeof(int64_t) * 102, static_cast<cudaStream_t>(stream)));
     if (d == 0) return RASP_OK;
     if (d > 0xffffffe0ull) return RASP_ECAPACITY;
     const uint32_t wb = in->word_bytes;
@@ -79,6 +87,7 @@ int rasp_run(const rasp_params *p, const rasp_batch *in, const rasp_batch *out, 
     a.in = side_of(in);
     a.out = side_of(out);
     a.tau_max = tau_max;
+    a.hist = reinterpret_cast<unsigned long long *>(hist);
     a.fresh = (flags & RASP_FRESH) ? 1 : 0;
     a.inplace = (in->iw == out->iw) ? 1 : 0;
     a.tile_rows = pl.tile_rows;

@@ -59,6 +59,7 @@ inline uint32_t max_epoch_len()
     return v;
 }
 constexpr int kWarpsPerBlockMax = RASP_BLOCK_WARPS;
+constexpr size_t kHistSmem = 512;       // block histogram (102 x u32) after the tiles, when requested
 constexpr size_t kBigTile = 16 * 1024;  // tiles above this use the one-warp, many-register kernel
 constexpr size_t kGlobalTileBudget = size_t(1) << 30;  // bytes of HBM tiles for huge n
 
@@ -226,16 +227,18 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
         // warps per block chosen to maximise resident warps per SM (ties: more
         // warps per block)
         LaunchShape sh;
-        const int rc = launch_shape(reinterpret_cast<const void *>(kern), dv, pl.tile_bytes, 0,
+        const size_t hist_bytes = base.hist ? kHistSmem : 0;
+        const int rc = launch_shape(reinterpret_cast<const void *>(kern), dv, pl.tile_bytes, hist_bytes,
                                     BIG ? 1 : kWarpsPerBlockMax, sh);
         if (rc) return rc;
         pl.warps_per_block = sh.units;
-        pl.dyn_smem = pl.tile_bytes * size_t(sh.units);
+        pl.dyn_smem = pl.tile_bytes * size_t(sh.units) + hist_bytes;
         pl.blocks = sh.per_sm * dv.nsm;
         if (std::getenv("RASP_DEBUG"))   // plan of this launch sequence (tuning aid)
             std::fprintf(stderr, "rasp: tile %zu B (%u rows), %d warps/block, %d blocks/SM, big %d\n",
                          pl.tile_bytes, pl.tile_rows, sh.units, sh.per_sm, int(BIG));
     }
+    else if (base.hist) pl.dyn_smem = kHistSmem;   // HBM tiles: only the histogram is in shared memory
     const int threads = 32 * pl.warps_per_block;
     const uint64_t tiles = (d + 31) / 32;
     const uint64_t need_blocks = (tiles + pl.warps_per_block - 1) / pl.warps_per_block;

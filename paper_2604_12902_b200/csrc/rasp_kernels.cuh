@@ -839,6 +839,14 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     const uint32_t ntiles = (K == 0 && !A.first) ? 0 : (count + 31) / 32;
     if (ntiles == 0) return;   // schedule finished: K[e+1] stays 0 from the memset
     const uint32_t nwarps = gridDim.x * (blockDim.x >> 5);
+    // the halting histogram of hypervisor.py:329-352, fused: every verdict
+    // lands in a block-private copy after the tiles in shared memory, flushed
+    // with one global atomic per non-empty bucket when the block ends
+    uint32_t *hist_s = reinterpret_cast<uint32_t *>(smem_raw + (SMEM ? (blockDim.x >> 5) * tile_bytes : 0u));
+    if (A.hist) {
+        for (uint32_t k = threadIdx.x; k < 102; k += blockDim.x) hist_s[k] = 0;
+        __syncthreads();
+    }
     const bool copy_side = A.first && !A.inplace;
     const bool fresh = A.fresh != 0;
 
@@ -885,6 +893,15 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const S *srcM = static_cast<const S *>(src.M) + id * n;
             const S *srcU = static_cast<const S *>(src.u) + id * ucols;
             const S *srcY = static_cast<const S *>(src.y) + id * ycols;
+            if (A.hist && valid && A.first && !running) {   // untouched: counted as it stands
+                const int8_t st0 = dst.status[id];
+                if (st0 == kHalted) {
+                    const int64_t th = dst.tau_h[id];
+                    atomicAdd(&hist_s[th < 100 ? static_cast<uint32_t>(th) : 100u], 1u);
+                } else if (st0 == kExhausted) {
+                    atomicAdd(&hist_s[101], 1u);
+                }
+            }
             if (valid && copy_side && !running) {
                 // untouched machine, out-of-place: carry i, a, M over (u, y are
                 // copied per tile above, or in bulk by the host for big tiles)
@@ -1047,6 +1064,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                     dst.status[id] = kHalted;
                     dst.tau_h[id] = tend;
                 }
+                if (A.hist) atomicAdd(&hist_s[!halted ? 101u : tend < 100 ? static_cast<uint32_t>(tend) : 100u], 1u);
             } else if (!fresh) {
                 dst.steps[id] = steps0 + K;
             }
@@ -1064,6 +1082,9 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
 
     // the last block to finish plans the next epoch
     __syncthreads();
+    if (A.hist)
+        for (uint32_t k = threadIdx.x; k < 102; k += blockDim.x)
+            if (hist_s[k]) atomicAdd(&A.hist[k], static_cast<unsigned long long>(hist_s[k]));
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(&sc->blocks_done[e], 1u) == gridDim.x - 1) {

@@ -143,11 +143,16 @@ class Engine:
 
     def run(self, batch: DeviceBatch, tau_max: int, epoch: int = 64,
             out: DeviceBatch | None = None, fresh: bool = False, stream=None,
-            workspace: torch.Tensor | None = None) -> DeviceBatch:
+            workspace: torch.Tensor | None = None, hist: torch.Tensor | None = None) -> DeviceBatch:
         """Phi to fixed point or tau_max for every RUNNING machine (rasp_run).
         In place unless `out` is given.  Asynchronous on `stream`.  Runs that
         may overlap on different streams need their own `workspace`
-        (workspace_bytes(d) bytes of device memory)."""
+        (workspace_bytes(d) bytes of device memory).  `hist` (device int64[102])
+        receives the batch's halting histogram, counted inside the run
+        (rasp_run_hist; the buckets of collect_histogram, hv:329-352)."""
+        if hist is not None and (hist.dtype != torch.int64 or hist.numel() != 102 or not hist.is_contiguous()
+                                 or hist.device != self.device):
+            raise ValueError("hist must be a contiguous int64[102] tensor on the engine's device")
         if tau_max < 0:
             raise ValueError(f"tau_max must be >= 0, got {tau_max}")
         if epoch < 1:
@@ -156,6 +161,8 @@ class Engine:
         if dst.d != batch.d or dst.word_bytes != batch.word_bytes:
             raise ValueError("out batch must match the input batch's size and word width")
         if batch.d == 0:
+            if hist is not None:
+                hist.zero_()
             return dst
         if workspace is not None:
             if workspace.numel() < self.workspace_bytes(batch.d):
@@ -165,10 +172,11 @@ class Engine:
             ws = self.workspace(batch.d)
         bi, bo = batch.c_struct(), dst.c_struct()
         with torch.cuda.device(self.device):
-            rc = self.lib.rasp_run(ctypes.byref(self._p), ctypes.byref(bi), ctypes.byref(bo),
-                                   int(tau_max), int(epoch),
-                                   _native.RASP_FRESH if fresh else 0,
-                                   ws.data_ptr(), ws.numel(), self._stream_ptr(stream))
+            rc = self.lib.rasp_run_hist(ctypes.byref(self._p), ctypes.byref(bi), ctypes.byref(bo),
+                                        int(tau_max), int(epoch),
+                                        _native.RASP_FRESH if fresh else 0,
+                                        hist.data_ptr() if hist is not None else None,
+                                        ws.data_ptr(), ws.numel(), self._stream_ptr(stream))
         _native.check(rc, "rasp_run")
         return dst
 

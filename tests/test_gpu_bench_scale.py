@@ -51,8 +51,10 @@ def _run_like_bench(torch, p, c0, tau, epoch):
     eng = get_engine(p, dev)
     src = DeviceBatch.from_arrays(c0, p, dev)
     dst = DeviceBatch.empty(src.d, p, dev, fresh=False)
-    eng.run(src, tau, epoch, out=dst, fresh=True)
+    fused = torch.empty(102, dtype=torch.int64, device=dev)
+    eng.run(src, tau, epoch, out=dst, fresh=True, hist=fused)
     hist = eng.histogram(dst).cpu().numpy()
+    np.testing.assert_array_equal(fused.cpu().numpy(), hist)   # counted in the run == re-read
     out = dst.to_numpy()
     return out, hist
 

@@ -101,6 +101,15 @@ def test_out_of_place_and_device_histogram(pkg, g):
         assert torch.equal(v, before[k]), k
     _assert_same(dst.to_numpy(), g, "out-of-place")
     assert list(eng.histogram(dst).cpu().numpy()) == list(g.hist)
+    # the histogram counted inside the run (rasp_run_hist), in and out of place
+    h = torch.full((102,), 7, dtype=torch.int64, device=dst.M.device)
+    dst2 = DeviceBatch.empty(g.d, p, fresh=False)
+    eng.run(src, g.tau_max, epoch=5, out=dst2, fresh=True, hist=h)
+    assert list(h.cpu().numpy()) == list(g.hist)
+    _assert_same(dst2.to_numpy(), g, "out-of-place, fused histogram")
+    h.fill_(3)
+    eng.run(src, g.tau_max, epoch=16, fresh=True, hist=h)
+    assert list(h.cpu().numpy()) == list(g.hist)
 
 
 def test_general_worker_contract(pkg):
@@ -129,6 +138,18 @@ def test_general_worker_contract(pkg):
             if k in FIELDS:
                 got = got.astype(np.uint64)
             np.testing.assert_array_equal(got, want[k], err_msg=f"{k} epoch={epoch}")
+    # the fused histogram counts machines that entered HALTED/EXHAUSTED as they stand
+    import torch
+    from paper_2604_12902_b200.engine import DeviceBatch
+    from paper_2604_12902_b200.sharding import histogram_np
+    arrays = {k: g.c0[k].astype(p.dtype) for k in FIELDS}
+    arrays.update(status=status, steps=steps, tau_h=tau_h)
+    for inplace in (True, False):
+        src = DeviceBatch.from_arrays(arrays, p)
+        dst = src if inplace else DeviceBatch.empty(d, p, fresh=False)
+        h = torch.zeros(102, dtype=torch.int64, device=src.M.device)
+        H.get_engine(p).run(src, g.tau_max, 8, out=dst, hist=h)
+        np.testing.assert_array_equal(h.cpu().numpy(), histogram_np(want["status"], want["tau_h"]))
 
 
 def test_bb_fixtures(pkg):
