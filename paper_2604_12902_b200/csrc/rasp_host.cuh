@@ -104,7 +104,10 @@ inline int raise_smem_limit_locked(const void *kern, const Device &dv)
 {
     static std::map<std::pair<const void *, int>, bool> raised;
     if (!raised[std::make_pair(kern, dv.id)]) {
-        RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, dv.smem_optin));
+        cudaFuncAttributes fa;
+        RASP_CUDA(cudaFuncGetAttributes(&fa, kern));   // static shared memory counts against the opt-in limit
+        RASP_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       dv.smem_optin - int(fa.sharedSizeBytes)));
         raised[std::make_pair(kern, dv.id)] = true;
     }
     return RASP_OK;
