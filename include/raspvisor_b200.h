@@ -41,6 +41,8 @@ extern "C" {
 #define RASP_EWORKSPACE -4  /* workspace too small */
 #define RASP_EDTYPE -5      /* word_bytes not in {1,2,4,8} or narrower than w */
 #define RASP_ENCCL -6       /* NCCL missing or an NCCL call failed; see rasp_last_cuda_error */
+#define RASP_ECHECK -7      /* checked build only: a kernel bounds/ownership check failed;
+                               details in rasp_last_cuda_error */
 
 /* VM status codes: hypervisor.py:63-69 */
 #define RASP_RUNNING 0
@@ -204,6 +206,10 @@ int rasp_shard_gather(void *comm, int root, const rasp_params *p, uint64_t d_tot
 /* Text for a RASP_E* code, and the last CUDA error string seen by this library. */
 const char *rasp_error_string(int code);
 const char *rasp_last_cuda_error(void);
+
+/* 1 if this library was built with the kernel bounds/ownership checks
+ * (-DRASP_CHECKED=1, the checked build tests/test_checked_build.py runs). */
+int rasp_checked_build(void);
 
 /* ABI version (RASP_ABI_VERSION) of the loaded library. */
 int rasp_abi_version(void);

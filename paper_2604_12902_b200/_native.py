@@ -26,7 +26,7 @@ EXPORTS = ("rasp_workspace_bytes", "rasp_run", "rasp_run_hist", "rasp_histogram"
            "rasp_launch_count", "rasp_enumerate", "rasp_init_c0", "rasp_generate",
            "rasp_pack", "rasp_unpack", "rasp_topk_workspace_bytes", "rasp_topk",
            "rasp_nccl_unique_id", "rasp_nccl_comm_init", "rasp_nccl_comm_destroy",
-           "rasp_shard_allreduce", "rasp_shard_gather")
+           "rasp_shard_allreduce", "rasp_shard_gather", "rasp_checked_build")
 
 RASP_GATHER_RESULTS = 1
 RASP_GATHER_OUTPUT = 2
@@ -86,6 +86,8 @@ def load():
     lib.rasp_error_string.restype = ctypes.c_char_p
     lib.rasp_last_cuda_error.argtypes = []
     lib.rasp_last_cuda_error.restype = ctypes.c_char_p
+    lib.rasp_checked_build.argtypes = []
+    lib.rasp_checked_build.restype = ctypes.c_int
     lib.rasp_abi_version.argtypes = []
     lib.rasp_abi_version.restype = ctypes.c_int
     lib.rasp_enumerate.argtypes = [ctypes.POINTER(RaspEnumParams), U64, U64, P, P, P]

@@ -16,6 +16,8 @@ extern "C" {
 
 int rasp_abi_version(void) { return RASP_ABI_VERSION; }
 
+int rasp_checked_build(void) { return RASP_CHECKED; }
+
 unsigned long long rasp_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char *rasp_error_string(int code)
@@ -28,6 +30,7 @@ const char *rasp_error_string(int code)
     case RASP_EWORKSPACE: return "workspace too small";
     case RASP_EDTYPE: return "word_bytes must be 1, 2, 4 or 8 and hold w bits";
     case RASP_ENCCL: return "NCCL unavailable or an NCCL call failed";
+    case RASP_ECHECK: return "kernel bounds/ownership check failed (checked build)";
     default: return "unknown error";
     }
 }
@@ -176,7 +179,7 @@ int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t cou
     kern<<<unsigned(grid), 256, smem, st>>>(a);
     RASP_CUDA(cudaGetLastError());
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    return RASP_OK;
+    return checked_result(st);
 }
 
 int rasp_init_c0(const rasp_params *p, const void *programs, uint32_t prog_len, const void *inputs,

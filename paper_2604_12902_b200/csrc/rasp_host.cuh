@@ -143,6 +143,30 @@ inline int launch_shape(const void *kern, const Device &dv, size_t unit_bytes, s
     return RASP_OK;
 }
 
+// Checked builds: wait for the launches on `st` and report the first kernel
+// check violation of this translation unit's kernels (g_check is per module).
+inline int checked_result(cudaStream_t st)
+{
+#if RASP_CHECKED
+    RASP_CUDA(cudaStreamSynchronize(st));
+    unsigned long long c[4] = {0, 0, 0, 0};
+    RASP_CUDA(cudaMemcpyFromSymbol(c, rasp::g_check, sizeof c));
+    if (c[0]) {
+        static const char *what[] = {"?", "shared access outside the dynamic window",
+                                     "cell access outside the lane's column", "machine index beyond the batch",
+                                     "output cursor beyond the tape", "list slot beyond the batch"};
+        std::snprintf(g_cuda_err, sizeof g_cuda_err, "check failed: %s (%llu, %llu; block %llu thread %llu)",
+                      what[c[0] < 6 ? c[0] : 0], c[1], c[2], c[3] >> 32, c[3] & 0xffffffffull);
+        const unsigned long long z[4] = {0, 0, 0, 0};
+        RASP_CUDA(cudaMemcpyToSymbol(rasp::g_check, z, sizeof z));
+        return RASP_ECHECK;
+    }
+#else
+    (void)st;
+#endif
+    return RASP_OK;
+}
+
 inline size_t natural_bytes(uint32_t w) { return w <= 8 ? 1 : w <= 16 ? 2 : w <= 32 ? 4 : 8; }
 inline size_t cell_bytes(uint32_t w) { return w <= 16 ? 2 : w <= 32 ? 4 : 8; }   // tile cell SC
 inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
@@ -316,7 +340,7 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
         RASP_CUDA(cudaGetLastError());
         g_launches.fetch_add(1, std::memory_order_relaxed);
     }
-    return RASP_OK;
+    return checked_result(st);
 }
 
 template <class S, class SC, class CT, bool POW2, rasp::Arith AR>

@@ -60,6 +60,54 @@ struct Side {
 
 constexpr int kMaxEpochs = 1024;
 
+// --- checked build (-DRASP_CHECKED=1): the stand-in for compute-sanitizer --------
+//
+// Every shared-memory access of the kernels is checked against the block's
+// dynamic shared window, every cell access of a step against the lane's own
+// column of its warp's tile (the lane-column layout's ownership rule: a lane
+// that touched another lane's cells would be a cross-thread hazard), and every
+// per-machine global row index against the batch.  The first violation is
+// recorded in g_check (code, two operands, thread); rasp_run of a checked
+// build synchronises and fails with RASP_ECHECK when one was seen.
+#ifndef RASP_CHECKED
+#define RASP_CHECKED 0
+#endif
+enum CheckCode : unsigned long long {
+    kChkSmemRange = 1,   // shared access outside the dynamic window
+    kChkColumn = 2,      // step cell access outside the lane's own column
+    kChkRow = 3,         // machine index beyond the batch
+    kChkYTape = 4,       // direct-to-HBM output cursor beyond the tape
+    kChkList = 5,        // compaction list slot beyond the batch
+};
+#if RASP_CHECKED
+static __device__ unsigned long long g_check[4];   // one per module (translation unit)
+extern __shared__ __align__(16) unsigned char rasp_dyn_smem[];
+static __device__ __noinline__ void check_fail(unsigned long long code, unsigned long long a, unsigned long long b)
+{
+    if (atomicCAS(&g_check[0], 0ull, code) == 0ull) {
+        g_check[1] = a;
+        g_check[2] = b;
+        g_check[3] = (static_cast<unsigned long long>(blockIdx.x) << 32) | threadIdx.x;
+    }
+}
+__device__ __forceinline__ void check_smem(uint32_t a, uint32_t bytes)
+{
+    uint32_t dsz;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dsz));
+    const uint32_t lo = static_cast<uint32_t>(__cvta_generic_to_shared(rasp_dyn_smem));
+    if (a < lo || a + bytes > lo + dsz) check_fail(kChkSmemRange, a, lo + dsz);
+}
+#define RASP_CHECK(cond, code, a, b) \
+    do {                             \
+        if (!(cond)) ::rasp::check_fail((code), (a), (b)); \
+    } while (0)
+#else
+__device__ __forceinline__ void check_smem(uint32_t, uint32_t) {}
+#define RASP_CHECK(cond, code, a, b) \
+    do {                             \
+    } while (0)
+#endif
+
 #ifndef RASP_UNROLL
 #define RASP_UNROLL 8
 #endif
@@ -187,9 +235,22 @@ __device__ __forceinline__ uint4 get16(const SC *col, uint32_t k)
 // Loads are issued in batches (8 x 16 B, or 8 scalars) before any of the
 // dependent shared-memory stores, so a row costs ~one DRAM latency instead
 // of one per chunk.
+// checked builds: the extent [col, col + ncells rows) lies in the dynamic window
+template <class SC>
+__device__ __forceinline__ void check_col_extent(const SC *col, uint32_t ncells)
+{
+#if RASP_CHECKED
+    if (ncells == 0 || !__isShared(col)) return;
+    const uint32_t a = static_cast<uint32_t>(__cvta_generic_to_shared(col));
+    check_smem(a, sizeof(SC));
+    check_smem(a + (ncells - 1) * 32 * static_cast<uint32_t>(sizeof(SC)), sizeof(SC));
+#endif
+}
+
 template <class S, class SC, uint32_t B = 8>
 __device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t ncells, SC *col)
 {
+    check_col_extent(col, ncells);
     constexpr uint32_t PER = 16 / sizeof(S);
     uint32_t k = 0;
     if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
@@ -216,6 +277,7 @@ __device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t nce
 template <class S, class SC>
 __device__ __forceinline__ void store_row(S *__restrict__ row, uint32_t ncells, const SC *col)
 {
+    check_col_extent(col, ncells);
     constexpr uint32_t PER = 16 / sizeof(S);
     uint32_t k = 0;
     if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
@@ -265,6 +327,7 @@ __device__ __forceinline__ uint32_t mx_addr(uint32_t tile0, uint32_t row0, uint3
 template <class SC>
 __device__ __forceinline__ void stsm(uint32_t addr, const uint4 v)
 {
+    check_smem(addr, 16);
     if constexpr (sizeof(SC) == 2)
         asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};"
                      ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
@@ -276,6 +339,7 @@ __device__ __forceinline__ void stsm(uint32_t addr, const uint4 v)
 template <class SC>
 __device__ __forceinline__ uint4 ldsm(uint32_t addr)
 {
+    check_smem(addr, 16);
     uint4 v;
     if constexpr (sizeof(SC) == 2)
         asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];"
@@ -460,6 +524,7 @@ template <class SC, class CT, bool SMEM>
 __device__ __forceinline__ CT ld_cell(char *base, uint32_t a)
 {
     if constexpr (SMEM) {
+        check_smem(a, sizeof(SC));
         if constexpr (sizeof(SC) == 2) {
             uint32_t v;   // zero-extending 16-bit load straight into a 32-bit register
             asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(a));
@@ -482,6 +547,7 @@ template <class SC, class CT, bool SMEM>
 __device__ __forceinline__ void st_cell(char *base, uint32_t a, CT v)
 {
     if constexpr (SMEM) {
+        check_smem(a, sizeof(SC));
         if constexpr (sizeof(SC) == 2) {
             asm volatile("st.shared.u16 [%0], %1;" ::"r"(a), "h"(static_cast<unsigned short>(v)) : "memory");
         } else if constexpr (sizeof(SC) == 4) {
@@ -508,6 +574,19 @@ struct Fetch {
     uint32_t jo;   // address of M[jw mod n]
 };
 
+// Lane-column ownership (checked builds): cell address `a` must be in the
+// column of the lane whose row-0 cell is at `lm`, within the tile's rows (M,
+// the input tape and its pad row, and the output rows when staged).
+template <class SC>
+__device__ __forceinline__ void check_col(uint32_t a, uint32_t lm, const Geo &g, bool yrows)
+{
+#if RASP_CHECKED
+    constexpr uint32_t ROW = 32 * sizeof(SC);
+    const uint32_t rows = g.n + g.ell + 1 + (yrows ? g.s : 0);
+    if (a < lm || (a - lm) % ROW != 0 || (a - lm) / ROW >= rows) check_fail(kChkColumn, a, lm);
+#endif
+}
+
 template <class SC, class CT, bool POW2, Arith AR, bool SMEM>
 __device__ __forceinline__ Fetch<CT> fetch(const LaneState<CT> &L, char *base, uint32_t lm,
                                            const Geo &g, const Opq &q)
@@ -523,9 +602,13 @@ __device__ __forceinline__ Fetch<CT> fetch(const LaneState<CT> &L, char *base, u
         ib = modn<CT, POW2>(wrap<CT, AR>(L.i + 1, mask), g);
     }
     Fetch<CT> f;
+    check_col<SC>((ia << SH) + lm, lm, g, false);
+    check_col<SC>((ib << SH) + lm, lm, g, false);
     f.o = ld_cell<SC, CT, SMEM>(base, (ia << SH) + lm);
     f.jw = ld_cell<SC, CT, SMEM>(base, (ib << SH) + lm);
     f.jo = (modn<CT, POW2>(f.jw, g) << SH) + lm;
+    check_col<SC>(f.jo, lm, g, false);
+    check_col<SC>(L.ua, lm, g, false);
     f.mj = ld_cell<SC, CT, SMEM>(base, f.jo);
     f.ud = ld_cell<SC, CT, SMEM>(base, L.ua);
     return f;
@@ -602,6 +685,7 @@ __device__ __forceinline__ void rasp_step(LaneState<CT> &L, char *base, uint32_t
             *reinterpret_cast<YS *>(ybase + L.ya) = static_cast<YS>(f.mj);
             L.ya += static_cast<uint32_t>(sizeof(YS));
         } else {
+            check_col<SC>(L.ya, lm, g, true);
             st_cell<SC, CT, SMEM>(base, L.ya, f.mj);
             L.ya += q.row;
         }
@@ -662,6 +746,7 @@ __device__ __forceinline__ void rasp_step_free(LaneState<CT> &L, char *base, uin
             L.ya += static_cast<uint32_t>(sizeof(YS));
         }
     } else if ((f.o == 7) & (L.ya < yend)) {
+        check_col<SC>(L.ya, lm, g, true);
         st_cell<SC, CT, SMEM>(base, L.ya, f.mj);
         L.ya += q.row;
     }
@@ -719,10 +804,14 @@ __device__ __forceinline__ void rasp_step_inc(LaneState<CT> &L, uint32_t &im, ui
     static_assert(AR != Arith::W1, "w = 1 uses the gated step");
     constexpr uint32_t SH = sizeof(SC) == 2 ? 6 : sizeof(SC) == 4 ? 7 : 8;   // log2(row bytes)
     const CT mask = static_cast<CT>(g.mask);
+    check_col<SC>((im << SH) + lm, lm, g, false);
+    check_col<SC>((ib << SH) + lm, lm, g, false);
     const CT o = ld_cell<SC, CT, SMEM>(base, (im << SH) + lm);
     const CT jw = ld_cell<SC, CT, SMEM>(base, (ib << SH) + lm);
     const uint32_t jn = modn<CT, false>(jw, g);
     const uint32_t jo = (jn << SH) + lm;
+    check_col<SC>(jo, lm, g, false);
+    check_col<SC>(L.ua, lm, g, false);
     const CT mj = ld_cell<SC, CT, SMEM>(base, jo);
     const CT ud = ld_cell<SC, CT, SMEM>(base, L.ua);
     const CT a0 = L.a;
@@ -756,6 +845,7 @@ __device__ __forceinline__ void rasp_step_inc(LaneState<CT> &L, uint32_t &im, ui
             L.ya += static_cast<uint32_t>(sizeof(YS));
         }
     } else if ((o == 7) & (L.ya < yend)) {
+        check_col<SC>(L.ya, lm, g, true);
         st_cell<SC, CT, SMEM>(base, L.ya, mj);
         L.ya += q.row;
     }
@@ -882,6 +972,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             const uint32_t j = tix * 32 + lane;
             const bool valid = j < count;
             const uint64_t id = valid ? (A.list_in ? A.list_in[j] : j) : 0;
+            RASP_CHECK(id < A.count_in, kChkRow, id, A.count_in);
             running = valid;
             int64_t steps0 = fresh ? covered : 0;
             if (valid && !fresh) {
@@ -1076,7 +1167,11 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                                 reinterpret_cast<const SC *>(gb + lm));
         if (sv) {
             sbase = __shfl_sync(kFull, sbase, 0);
-            if (survivor) A.list_out[sbase + __popc(sv & ((1u << lane) - 1u))] = static_cast<uint32_t>(id);
+            if (survivor) {
+                RASP_CHECK(sbase + __popc(sv & ((1u << lane) - 1u)) < A.count_in, kChkList,
+                           sbase + __popc(sv & ((1u << lane) - 1u)), A.count_in);
+                A.list_out[sbase + __popc(sv & ((1u << lane) - 1u))] = static_cast<uint32_t>(id);
+            }
         }
     }
 
@@ -1201,6 +1296,7 @@ enum_kernel(const EnumArgs A)
                     cell = (k & 1) ? (pair >> A.ob) : (pair & ((1u << A.ob) - 1u));
                 }
                 const uint32_t w2 = cell | (cell << 16);
+                check_smem(tile0 + k * ROW + (c & 3) * 16, 16);
                 asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(tile0 + k * ROW + (c & 3) * 16), "r"(w2)
                              : "memory");
             }

@@ -1,10 +1,16 @@
-"""Small workloads for compute-sanitizer runs (tests/test_sanitizer.py).
+"""Small workloads for the checked build of the engine (tests/test_checked_build.py).
 
-    compute-sanitizer --tool memcheck|racecheck|synccheck python tests/sanitize_workload.py <kind>
+    RASP_LIBRARY=paper_2604_12902_b200/_lib/libraspvisor_b200_checked.so \
+        python tests/check_workload.py <kind>
 
-Each kind launches one family of the engine's kernels on a batch small enough
-for the sanitizer's instrumentation (~100x slowdown) and checks the results
-against the CPU oracle, so a run that is clean but wrong also fails.
+compute-sanitizer is closed on the GPU pool this project runs on (runs under
+it left GPUs needing a reset), so its checks are compiled into the kernels
+instead (-DRASP_CHECKED=1, csrc/rasp_kernels.cuh): every shared access within
+the block's dynamic window, every cell access of a step within the lane's own
+column (the ownership rule that makes the tiles race-free), every machine
+index and compaction slot within the batch.  Each kind launches one family of
+the engine's kernels and checks the results against the CPU oracle, so a run
+that passes the checks but is wrong also fails.
 Kinds:
   mx      u16 cells, lane-column tiles moved with stmatrix/ldmatrix (C2 shape),
           out of place (tile-wise u/y copies) and in place
@@ -147,7 +153,8 @@ def main(kind):
     else:
         raise SystemExit(f"unknown kind {kind}")
     torch.cuda.synchronize()
-    print(f"sanitize workload {kind}: ok")
+    from paper_2604_12902_b200 import _native
+    print(f"check workload {kind}: ok (checked build: {_native.load().rasp_checked_build()})")
 
 
 if __name__ == "__main__":
