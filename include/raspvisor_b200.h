@@ -134,10 +134,11 @@ int rasp_generate(const rasp_params *p, uint64_t seed, uint64_t first_machine,
  * init_config(P_r, [x]) (machine.py:289-309) with ell = s = 1, for every
  * input word x in [0, 2^w), run for at most tau_max steps.  Per program, one
  * record: bit 63 = every input reached a fixed point within tau_max; bits
- * 0..62 = sum over x of mix64(x | halted<<8 | y0<<9 | y1<<10 | tau_h<<18)
- * (splitmix64 finaliser; y1 and tau_h count only when written / halted).
- * records: uint64[count] device buffer; steps_total: device counter that
- * accumulates the applied machine-steps.  2 <= w <= 8. */
+ * 0..62 = sum over x of fmix32(x | halted<<8 | y0<<9 | y1<<10 | tau_h<<18)
+ * (murmur3's 32-bit finaliser of a 32-bit key; y1 and tau_h count only when
+ * written / halted).  records: uint64[count] device buffer; steps_total:
+ * device counter that accumulates the applied machine-steps.  2 <= w <= 8,
+ * tau_max < 2^14. */
 typedef struct rasp_enum_params {
     uint32_t m;             /* instruction pairs */
     uint32_t opcode_bits;   /* ob */

@@ -232,12 +232,15 @@ int oracle_step(u64 *i, u64 *a, u64 *M, u64 *u, u64 *y,
  * Same machine semantics (oracle_advance) driven per (program rank, input x),
  * run_to_fixpoint style (machine.py:336-357) with budget tau; the per-program
  * record definition mirrors include/raspvisor_b200.h (rasp_enumerate). */
-static uint64_t mix64(uint64_t z)
+/* murmur3's 32-bit finaliser: the per-input fingerprint of a record */
+static uint32_t fmix32(uint32_t h)
 {
-    z += 0x9e3779b97f4a7c15ull;
-    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
-    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
-    return z ^ (z >> 31);
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
 }
 
 typedef struct {
@@ -282,7 +285,7 @@ static void *enum_main(void *p)
             if (!halted) all = 0;
             const u64 key = x | ((u64)halted << 8) | (y[0] << 9) | ((y[0] ? y[1] : 0) << 10) |
                             ((u64)(halted ? t : 0) << 18);
-            sum += mix64(key);
+            sum += fmix32((uint32_t)key);
         }
         a->records[pi] = ((u64)all << 63) | (sum & 0x7fffffffffffffffull);
     }

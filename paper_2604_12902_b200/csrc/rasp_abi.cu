@@ -139,6 +139,7 @@ int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t cou
         ep->operand_bits < 1 || ep->opcode_bits > ep->w || ep->operand_bits > ep->w ||
         uint64_t(ep->m) * (ep->opcode_bits + ep->operand_bits) > 63)
         return RASP_EPARAM;
+    if (ep->tau_max >= (1u << 14)) return RASP_EPARAM;   // tau_h must fit the record key's 14 bits
     if (2 * ep->m > ep->n) return RASP_ECAPACITY;
     if (count == 0) return RASP_OK;
     Device dv;
@@ -161,9 +162,14 @@ int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t cou
     a.ob = ep->opcode_bits;
     a.pb = ep->operand_bits;
     a.tau = ep->tau_max;
-    const size_t smem = size_t(8) * (ep->n + 3) * 64;
+    // per warp: its tile (n + 3 rows of 32 u16 cells) + the program (n cells)
+    const size_t smem = size_t(8) * ((ep->n + 3) * 64 + ((2 * ep->n + 15) & ~15u));
     const bool pow2 = (ep->n & (ep->n - 1)) == 0;
-    auto kern = pow2 ? rasp::enum_kernel<true, rasp::Arith::NARROW> : rasp::enum_kernel<false, rasp::Arith::NARROW>;
+    // steps between lane checks: 2, or 1 when tau_max is odd (machines start at
+    // checks and must reach their budget exactly at one)
+    const bool even = (ep->tau_max & 1) == 0;
+    auto kern = pow2 ? (even ? rasp::enum_kernel<true, rasp::Arith::NARROW, 2> : rasp::enum_kernel<true, rasp::Arith::NARROW, 1>)
+                     : (even ? rasp::enum_kernel<false, rasp::Arith::NARROW, 2> : rasp::enum_kernel<false, rasp::Arith::NARROW, 1>);
     if (smem > size_t(dv.smem_optin)) return RASP_ECAPACITY;
     int per_sm = 0;
     {

@@ -1224,12 +1224,16 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
 // Program rank r in [0, 2^(m*(ob+pb))): pair k occupies bits [k*(ob+pb), ...)
 // of r, opcode = low ob bits, operand = next pb bits.  Machine (r, x) is
 // c0(P_r, (x)) with ell = s = 1 and x in [0, 2^w) (init_config, m:289-309).
-// One block runs one program on all 2^w inputs (w <= 8: 256 lanes), each
-// warp on 32 of them, with the same tile/step code as the batch engine, then
-// reduces the inputs into one 64-bit record:
+// A warp takes whole programs; its lanes take the program's inputs one after
+// the other: a lane whose machine stopped (fixed point or budget) folds it
+// into the record, claims the next input of the program and restores its own
+// column of the tile to the program (the columns are independent machines),
+// so no lane waits for the slowest input of a group.  Per program one record:
 //   bit 63     all inputs reached a fixed point within tau_max
-//   bits 0..62 sum over x of mix64(x | halted << 8 | y0 << 9 | y1 << 10 | tau_h << 18)
-// (a sum, so the reduction order cannot change it).
+//   bits 0..62 sum over x of fmix32(x | halted << 8 | y0 << 9 | y1 << 10 | tau_h << 18)
+// (a sum, so the order the lanes finish in cannot change it; y1 and tau_h
+// count only when written / halted; the key fits 32 bits for w <= 8 and
+// tau_max < 2^14).
 
 struct EnumArgs {
     Geo g;
@@ -1249,13 +1253,21 @@ __device__ __forceinline__ uint64_t mix64(uint64_t z)
     return z ^ (z >> 31);
 }
 
-template <bool POW2, Arith AR>
-__global__ void __launch_bounds__(256)
+// murmur3's 32-bit finaliser: the per-input fingerprint of the C4 records
+__device__ __forceinline__ uint32_t fmix32(uint32_t h)
+{
+    h ^= h >> 16;
+    h *= 0x85ebca6bu;
+    h ^= h >> 13;
+    h *= 0xc2b2ae35u;
+    h ^= h >> 16;
+    return h;
+}
+
+template <bool POW2, Arith AR, uint32_t UN>
+__global__ void __launch_bounds__(256, 5)
 enum_kernel(const EnumArgs A)
 {
-    // Each warp takes whole programs: the 2^w inputs of a program run as
-    // groups of 32 lanes on the warp's tile, one after the other, and the warp
-    // alone reduces them into the program's record (no block barriers).
     using SC = uint16_t;
     using CT = uint32_t;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1266,80 +1278,105 @@ enum_kernel(const EnumArgs A)
     const Geo g = A.g;
     const uint32_t n = g.n;
     const uint32_t tile_bytes = (n + 3) * ROW;     // M, u[1] + pad, y[1]
+    const uint32_t prog_bytes = (2 * n + 15) & ~15u;   // the program, machine-major
     char *tb = reinterpret_cast<char *>(smem_raw);
-    const uint32_t tile0 = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw)) + wib * tile_bytes;
+    const uint32_t s0 = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+    const uint32_t nwb = blockDim.x >> 5;
+    const uint32_t tile0 = s0 + wib * tile_bytes;
+    const uint32_t prog0 = s0 + nwb * tile_bytes + wib * prog_bytes;
     const uint32_t lm = tile0 + lane * static_cast<uint32_t>(sizeof(SC));
-    char *gb = reinterpret_cast<char *>(smem_raw) - static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
     const uint32_t U = n * ROW + lm, Y = (n + 2) * ROW + lm;
     const uint32_t uend = U + ROW, yend = Y + ROW;
     const Opq q = {1u, 2u, ROW};
     const uint32_t pw = A.ob + A.pb;
     const uint32_t xs = static_cast<uint32_t>(g.mask) + 1;   // inputs per program (2^w)
-    const uint32_t groups = (xs + 31) / 32;
-    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * (blockDim.x >> 5);
+    const uint32_t K = A.tau;
+    const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * nwb;
     unsigned long long my_steps = 0;
 
-    for (uint64_t pi = blockIdx.x * static_cast<uint64_t>(blockDim.x >> 5) + wib; pi < A.count; pi += nwarps) {
+    for (uint64_t pi = blockIdx.x * static_cast<uint64_t>(nwb) + wib; pi < A.count; pi += nwarps) {
         const uint64_t r = A.first + pi;
+        // the program, once per program, machine-major (lane c writes cell c)
+        for (uint32_t c = lane; c < n; c += 32) {
+            uint32_t cell = 0;
+            if (c < 2 * A.m) {
+                const uint32_t pair = static_cast<uint32_t>(r >> ((c >> 1) * pw)) & ((1u << pw) - 1u);
+                cell = (c & 1) ? (pair >> A.ob) : (pair & ((1u << A.ob) - 1u));
+            }
+            st_cell<SC, CT, true>(tb, prog0 + 2 * c, cell);
+        }
+        __syncwarp();
         uint64_t v = 0;
         bool all_halted = true;
-        for (uint32_t grp = 0; grp < groups; ++grp) {
-            const uint32_t x = grp * 32 + lane;               // the input word of this lane
-            const bool valid_x = x < xs;
-            // c0: every lane holds the same program, so the warp writes the
-            // M rows 16 bytes at a time (row k = 8 copies of cell k per 16 B)
-            for (uint32_t c = lane; c < 4 * n; c += 32) {
-                const uint32_t k = c >> 2;
-                uint32_t cell = 0;
-                if (k < 2 * A.m) {
-                    const uint32_t pair = static_cast<uint32_t>(r >> ((k >> 1) * pw)) & ((1u << pw) - 1u);
-                    cell = (k & 1) ? (pair >> A.ob) : (pair & ((1u << A.ob) - 1u));
+        uint32_t next = 32;      // next input to hand out (warp-uniform)
+        uint32_t x = lane;       // this lane's input
+        bool has = x < xs;
+        LaneState<CT> L;
+        L.tlast = 0;
+        L.active = false;
+        // (re)start the lane's machine on input x: its column = the program,
+        // u[1] = x, empty output tape
+        auto start = [&](bool go) {
+            if (go) {
+                uint32_t c = 0;
+                for (; c + 8 <= n; c += 8) {   // 8 program cells per 16-byte broadcast read
+                    uint4 v8;
+                    check_smem(prog0 + 2 * c, 16);
+                    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                                 : "=r"(v8.x), "=r"(v8.y), "=r"(v8.z), "=r"(v8.w) : "r"(prog0 + 2 * c));
+                    const uint32_t w4[4] = {v8.x, v8.y, v8.z, v8.w};
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        st_cell<SC, CT, true>(tb, lm + (c + 2 * e) * ROW, w4[e] & 0xffffu);
+                        st_cell<SC, CT, true>(tb, lm + (c + 2 * e + 1) * ROW, w4[e] >> 16);
+                    }
                 }
-                const uint32_t w2 = cell | (cell << 16);
-                check_smem(tile0 + k * ROW + (c & 3) * 16, 16);
-                asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(tile0 + k * ROW + (c & 3) * 16), "r"(w2)
-                             : "memory");
+                for (; c < n; ++c)
+                    st_cell<SC, CT, true>(tb, lm + c * ROW, ld_cell<SC, CT, true>(tb, prog0 + 2 * c));
+                st_cell<SC, CT, true>(tb, U, x);
+            } else {
+                st_cell<SC, CT, true>(tb, lm, 0u);   // parked: opcode 0 at i = 0, a fixed point
             }
-            st_cell<SC, CT, true>(tb, U, x);   // u[1] = x
-            __syncwarp();
-            LaneState<CT> L;
-            L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tlast = 0; L.rem = A.tau;
-            L.active = true;
-            const uint32_t K = A.tau;
-            uint32_t t = 0;
-            bool live = true;
-            for (; live && t + 2 <= K; t += 2) {
-                rasp_step_free<SC, CT, POW2, AR, true>(L, tb, lm, uend, yend, g, q);
-                rasp_step_free<SC, CT, POW2, AR, true>(L, tb, lm, uend, yend, g, q);
-                live = __any_sync(kFull, valid_x & L.active);
+            L.i = 0; L.a = 0; L.ua = U; L.ya = Y; L.tlast = 0; L.rem = K;
+            L.active = go;
+        };
+        start(has);
+        for (;;) {
+            // UN steps (machines start at check boundaries and tau_max % UN == 0,
+            // so a live lane reaches its budget exactly at a check)
+            if (K > 0) {
+#pragma unroll
+                for (uint32_t t = 0; t < UN; ++t) rasp_step_free<SC, CT, POW2, AR, true>(L, tb, lm, uend, yend, g, q);
             }
-            if (live && t < K) {
-                rasp_step_free<SC, CT, POW2, AR, true>(L, tb, lm, uend, yend, g, q);
-                ++t;
-            }
-            if (valid_x) {
-                // tlast = moves: below K the machine stopped at a fixed point;
-                // at K it is fixed there or out of budget
-                bool halted = L.tlast < K;
-                if (!halted) {
-                    const Fetch<CT> f = fetch<SC, CT, POW2, AR, true>(L, tb, lm, g, q);
-                    halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, g, q);
+            // lanes whose machine stopped moving (fixed point) or used its budget
+            const bool done = has && (!L.active || L.tlast == K);
+            const unsigned dm = __ballot_sync(kFull, done);
+            if (dm) {
+                if (done) {
+                    bool halted = L.tlast < K || !L.active;
+                    if (L.tlast == K) {   // at the budget: the final probe (hv:140-148)
+                        const Fetch<CT> f = fetch<SC, CT, POW2, AR, true>(L, tb, lm, g, q);
+                        halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, g, q);
+                    }
+                    const uint32_t y0 = (L.ya - Y) / ROW;
+                    const uint32_t y1 = y0 ? static_cast<uint32_t>(ld_cell<SC, CT, true>(tb, Y)) : 0u;
+                    const uint32_t key = x | (static_cast<uint32_t>(halted) << 8) | (y0 << 9) | (y1 << 10) |
+                                         ((halted ? L.tlast : 0u) << 18);
+                    v += fmix32(key);
+                    all_halted &= halted;
+                    my_steps += L.tlast;
+                    x = next + __popc(dm & ((1u << lane) - 1u));
+                    has = x < xs;
+                    start(has);
                 }
-                const uint32_t y0 = (L.ya - Y) / ROW;
-                const uint32_t y1 = *reinterpret_cast<const SC *>(gb + Y);   // y[1] (0 unless written)
-                const uint64_t key = static_cast<uint64_t>(x) | (static_cast<uint64_t>(halted) << 8) |
-                                     (static_cast<uint64_t>(y0) << 9) |
-                                     (static_cast<uint64_t>(y0 ? y1 : 0u) << 10) |
-                                     (static_cast<uint64_t>(halted ? L.tlast : 0u) << 18);
-                v += mix64(key);
-                all_halted &= halted;
-                my_steps += L.tlast;
+                next += __popc(dm);
             }
-            __syncwarp();   // the next group rewrites every column
+            if (!__any_sync(kFull, has)) break;
         }
         for (int off = 16; off; off >>= 1) v += __shfl_down_sync(kFull, v, off);
         const unsigned all = __all_sync(kFull, all_halted);
         if (lane == 0) A.records[pi] = (static_cast<uint64_t>(all != 0) << 63) | (v & 0x7fffffffffffffffull);
+        __syncwarp();   // the next program rewrites the program area
     }
     // machine-steps: one atomic per block
     for (int off = 16; off; off >>= 1) my_steps += __shfl_down_sync(kFull, my_steps, off);
@@ -1390,8 +1427,6 @@ __global__ void init_c0_kernel(Side b, uint64_t d, uint32_t n, uint32_t ell, uin
         b.tau_h[j] = -1;
     }
 }
-
-__device__ __forceinline__ uint64_t mix64(uint64_t z);
 
 template <class S>
 __global__ void generate_kernel(Side b, uint64_t d, uint64_t first, uint32_t n, uint32_t ell,

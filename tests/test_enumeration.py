@@ -13,11 +13,12 @@ REDUCED = EnumDomain(m=3, opcode_bits=3, operand_bits=3, w=8, n=8, tau_max=64)
 MASK63 = (1 << 63) - 1
 
 
-def _mix64(z):
-    z = (z + 0x9E3779B97F4A7C15) & 0xFFFFFFFFFFFFFFFF
-    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & 0xFFFFFFFFFFFFFFFF
-    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & 0xFFFFFFFFFFFFFFFF
-    return z ^ (z >> 31)
+def _fmix32(h):
+    h ^= h >> 16
+    h = (h * 0x85EBCA6B) & 0xFFFFFFFF
+    h ^= h >> 13
+    h = (h * 0xC2B2AE35) & 0xFFFFFFFF
+    return h ^ (h >> 16)
 
 
 def _record_scalar(dom, rank):
@@ -33,7 +34,8 @@ def _record_scalar(dom, rank):
         y0, y1 = cf[4]
         key = x | (int(halted) << 8) | (y0 << 9) | ((y1 if y0 else 0) << 10) | \
             ((tau if halted else 0) << 18)
-        total = (total + _mix64(key)) & 0xFFFFFFFFFFFFFFFF
+        assert key < 1 << 32
+        total = (total + _fmix32(key)) & 0xFFFFFFFFFFFFFFFF
         steps += tau if halted else dom.tau_max
     return (int(allh) << 63) | (total & MASK63), steps
 
