@@ -742,7 +742,12 @@ def bench_batch(args, world, rank, local_rank, dev):
         dist.destroy_process_group()
         return
 
-    roof = roofline(machine_steps, d, w, n, ell, s, t_kernel)
+    # one GPU: the timed region IS the kernel sequence of rasp_run_hist (graph
+    # replays), so the roofline uses it; N > 1 adds collectives to the step,
+    # so there the separately timed eager run is used
+    roof = roofline(machine_steps, d, w, n, ell, s, t_step if world == 1 else t_kernel)
+    roof["timed"] = "graph replays of rasp_run_hist (the timed region)" if world == 1 and graph is not None \
+        else "eager rasp_run (CUDA events around its launches)"
     roof["traffic"], roof["traffic_detail"] = _traffic(args.config) if world == 1 else (None, None)
     line = {
         "metric": "machine-steps/s", "value": total_steps / t_step, "unit": "machine-steps/s", "n_gpus": world,

@@ -167,7 +167,10 @@ int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t cou
     const bool pow2 = (ep->n & (ep->n - 1)) == 0;
     // steps between lane checks: 2, or 1 when tau_max is odd (machines start at
     // checks and must reach their budget exactly at one)
-    const bool even = (ep->tau_max & 1) == 0;
+#ifndef RASP_ENUM_CHECK
+#define RASP_ENUM_CHECK 2
+#endif
+    const bool even = RASP_ENUM_CHECK == 2 && (ep->tau_max & 1) == 0;
     auto kern = pow2 ? (even ? rasp::enum_kernel<true, rasp::Arith::NARROW, 2> : rasp::enum_kernel<true, rasp::Arith::NARROW, 1>)
                      : (even ? rasp::enum_kernel<false, rasp::Arith::NARROW, 2> : rasp::enum_kernel<false, rasp::Arith::NARROW, 1>);
     if (smem > size_t(dv.smem_optin)) return RASP_ECAPACITY;
