@@ -587,7 +587,9 @@ __device__ __forceinline__ void check_col(uint32_t a, uint32_t lm, const Geo &g,
 #endif
 }
 
-template <class SC, class CT, bool POW2, Arith AR, bool SMEM>
+// LAZY_UD: skip the input-tape read (the ungated steps read u[u0+1] only
+// when the instruction is an RD that will store it)
+template <class SC, class CT, bool POW2, Arith AR, bool SMEM, bool LAZY_UD = false, bool LAZY_MJ = false>
 __device__ __forceinline__ Fetch<CT> fetch(const LaneState<CT> &L, char *base, uint32_t lm,
                                            const Geo &g, const Opq &q)
 {
@@ -609,10 +611,26 @@ __device__ __forceinline__ Fetch<CT> fetch(const LaneState<CT> &L, char *base, u
     f.jo = (modn<CT, POW2>(f.jw, g) << SH) + lm;
     check_col<SC>(f.jo, lm, g, false);
     check_col<SC>(L.ua, lm, g, false);
-    f.mj = ld_cell<SC, CT, SMEM>(base, f.jo);
-    f.ud = ld_cell<SC, CT, SMEM>(base, L.ua);
+    if constexpr (!LAZY_MJ) f.mj = ld_cell<SC, CT, SMEM>(base, f.jo);
+    if constexpr (!LAZY_UD) f.ud = ld_cell<SC, CT, SMEM>(base, L.ua);
+    else f.ud = 0;
     return f;
 }
+
+// Read the input tape lazily in the ungated steps of shared-memory tiles: one
+// shared load fewer per step for the 6 of 7 instructions that are not RD
+// (measured on the ALU/MIO-bound small tiles; the latency-bound big tiles keep
+// the early read, which overlaps the fetch)
+#ifndef RASP_LAZY_UD
+#define RASP_LAZY_UD 1
+#endif
+template <bool YG>
+constexpr bool kLazyUd = RASP_LAZY_UD && !YG;
+#ifndef RASP_LAZY_MJ
+#define RASP_LAZY_MJ 0
+#endif
+template <bool YG>
+constexpr bool kLazyMj = RASP_LAZY_MJ && !YG;
 
 // Fixedness (hv:115): the next configuration equals the current one.  For
 // w >= 2, (i+2) mod 2^w != i, so every advancing case moves i and the test
@@ -722,7 +740,9 @@ __device__ __forceinline__ void rasp_step_free(LaneState<CT> &L, char *base, uin
 {
     static_assert(AR != Arith::W1, "w = 1 uses the gated step");
     const CT mask = static_cast<CT>(g.mask);
-    const Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM>(L, base, lm, g, q);
+    Fetch<CT> f = fetch<SC, CT, POW2, AR, SMEM, kLazyUd<YG>, kLazyMj<YG>>(L, base, lm, g, q);
+    if constexpr (kLazyMj<YG>)   // M[j] only for the instructions that use it
+        f.mj = ((f.o == 2) | (f.o == 3) | (f.o == 7)) ? ld_cell<SC, CT, SMEM>(base, f.jo) : CT(0);
     const CT a0 = L.a;
     const bool ucap = L.ua >= uend;
     const bool taken = (f.o == 5) & ((AR == Arith::CELL ? (a0 & mask) : a0) != 0);
@@ -737,7 +757,7 @@ __device__ __forceinline__ void rasp_step_free(LaneState<CT> &L, char *base, uin
     }
     if (f.o == 4) st_cell<SC, CT, SMEM>(base, f.jo, a0);
     if ((f.o == 6) & !ucap) {
-        st_cell<SC, CT, SMEM>(base, f.jo, f.ud);
+        st_cell<SC, CT, SMEM>(base, f.jo, kLazyUd<YG> ? ld_cell<SC, CT, SMEM>(base, L.ua) : f.ud);
         L.ua += q.row;
     }
     if constexpr (YG) {   // HBM row: lanes without a machine must not store
@@ -812,8 +832,8 @@ __device__ __forceinline__ void rasp_step_inc(LaneState<CT> &L, uint32_t &im, ui
     const uint32_t jo = (jn << SH) + lm;
     check_col<SC>(jo, lm, g, false);
     check_col<SC>(L.ua, lm, g, false);
-    const CT mj = ld_cell<SC, CT, SMEM>(base, jo);
-    const CT ud = ld_cell<SC, CT, SMEM>(base, L.ua);
+    const CT mj = (!kLazyMj<YG> || (o == 2) | (o == 3) | (o == 7)) ? ld_cell<SC, CT, SMEM>(base, jo) : CT(0);
+    const CT ud = kLazyUd<YG> ? CT(0) : ld_cell<SC, CT, SMEM>(base, L.ua);
     const CT a0 = L.a;
     const bool ucap = L.ua >= uend;
     const bool taken = (o == 5) & ((AR == Arith::CELL ? (a0 & mask) : a0) != 0);
@@ -836,7 +856,7 @@ __device__ __forceinline__ void rasp_step_inc(LaneState<CT> &L, uint32_t &im, ui
     }
     if (o == 4) st_cell<SC, CT, SMEM>(base, jo, a0);
     if ((o == 6) & !ucap) {
-        st_cell<SC, CT, SMEM>(base, jo, ud);
+        st_cell<SC, CT, SMEM>(base, jo, kLazyUd<YG> ? ld_cell<SC, CT, SMEM>(base, L.ua) : ud);
         L.ua += q.row;
     }
     if constexpr (YG) {   // HBM row: lanes without a machine (no ybase) must not store
@@ -958,7 +978,9 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 // (identity list), so their u and y rows are two contiguous
                 // blocks -- copy them to `out` here, before any write-back of
                 // this tile touches them (replaces a bulk copy kernel per tape;
-                // the latency-bound big tiles keep the bulk copies: measured)
+                // the latency-bound big tiles keep the bulk copies: measured;
+                // deferring the copy to the write-back behind an L2 prefetch
+                // measured +0.2% on C2/C3)
                 const uint64_t m0 = static_cast<uint64_t>(tix) * 32;
                 const uint64_t m1 = min(static_cast<uint64_t>(count), m0 + 32);
                 warp_copy(static_cast<S *>(dst.u) + m0 * ucols, static_cast<const S *>(A.in.u) + m0 * ucols,
