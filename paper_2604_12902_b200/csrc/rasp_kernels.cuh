@@ -1356,7 +1356,13 @@ enum_kernel(const EnumArgs A)
     const uint64_t nwarps = static_cast<uint64_t>(gridDim.x) * nwb;
     unsigned long long my_steps = 0;
 
-    for (uint64_t pi = blockIdx.x * static_cast<uint64_t>(nwb) + wib; pi < A.count; pi += nwarps) {
+    // programs go to warps in groups of 4 consecutive ranks, so a warp writes
+    // its 4 records as one 32-byte sector (8-byte records from different warps
+    // left partial sectors for L2 to merge: 14 GB of DRAM traffic for 2 GB of
+    // records)
+    uint64_t myrec = 0;   // lane k < 4: the record of program k of the current group
+    for (uint64_t pi = (blockIdx.x * static_cast<uint64_t>(nwb) + wib) * 4; pi < A.count;
+         pi += ((pi & 3) == 3) ? 4 * nwarps - 3 : 1) {
         const uint64_t r = A.first + pi;
         // the program, once per program, machine-major (lane c writes cell c)
         for (uint32_t c = lane; c < n; c += 32) {
@@ -1435,9 +1441,14 @@ enum_kernel(const EnumArgs A)
             }
             if (!__any_sync(kFull, has)) break;
         }
-        for (int off = 16; off; off >>= 1) v += __shfl_down_sync(kFull, v, off);
+        for (int off = 16; off; off >>= 1) v += __shfl_xor_sync(kFull, v, off);
         const unsigned all = __all_sync(kFull, all_halted);
-        if (lane == 0) A.records[pi] = (static_cast<uint64_t>(all != 0) << 63) | (v & 0x7fffffffffffffffull);
+        if (lane == static_cast<uint32_t>(pi & 3))
+            myrec = (static_cast<uint64_t>(all != 0) << 63) | (v & 0x7fffffffffffffffull);
+        // a full group (or the batch's last program): lanes 0-3 write the
+        // group's records, one sector
+        if (((pi & 3) == 3 || pi + 1 == A.count) && lane <= static_cast<uint32_t>(pi & 3))
+            A.records[(pi & ~uint64_t(3)) + lane] = myrec;
         __syncwarp();   // the next program rewrites the program area
     }
     // machine-steps: one atomic per block
