@@ -3,6 +3,7 @@ histograms and the slot view (mirrors tests/test_machine.py:21-79 and
 tests/test_hypervisor.py:107-171 of the reference)."""
 
 import json
+import os
 
 import numpy as np
 import pytest
@@ -168,3 +169,36 @@ def test_product_never_imports_oracle():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "import oracle" not in text and "from oracle" not in text, f
+
+
+def test_dropin_routes_the_reference_run_batch_without_cpu_fallback():
+    """dropin.install makes the reference's run_batch (baseline/_ref) call the
+    C-ABI engine; without a GPU that call fails loudly (no CPU fallback)."""
+    import importlib
+    import sys
+
+    ref = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref, "raspvisor")):
+        pytest.skip("the reference is not staged in baseline/_ref")
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/raspvisor_numba_cache")
+    sys.path.insert(0, ref)
+    try:
+        RH = importlib.import_module("raspvisor.hypervisor")
+        RM = importlib.import_module("raspvisor.machine")
+        from paper_2604_12902_b200 import dropin
+        from paper_2604_12902_b200.errors import NativeError
+        original = RH._worker
+        dropin.install(RH)
+        try:
+            assert RH._worker is dropin.worker
+            p = RM.MachineParams(w=8, n=8, ell=2, s=2, mu=1)
+            c = RM.init_config(RM.Program((1, 5, 4, 6)), [], p)
+            import torch
+            if torch.cuda.is_available():
+                pytest.skip("GPU present: covered by tests/test_dropin_reference.py")
+            with pytest.raises((NativeError, RuntimeError, AssertionError)):
+                RH.run_batch([c], p, RH.BatchConfig(tau_max=8, workers=1))
+        finally:
+            RH._worker = original
+    finally:
+        sys.path.remove(ref)
