@@ -27,11 +27,12 @@ import torch
 
 from .engine import ALL_FIELDS, WORD_FIELDS, DeviceBatch, Engine
 from .errors import CapacityError
-from .machine import Config, MachineParams, validate_config
+from .machine import Config, MachineParams, init_config, validate_config
 
 __all__ = [
     "VmStatus", "BatchConfig", "VmSlot", "SlotView", "BatchResult", "run_batch",
     "run_arrays", "run_device", "run_programs", "collect_histogram", "HISTOGRAM_KEYS", "get_engine",
+    "Workload", "build_workload_from_programs", "throughput_bench",
 ]
 
 _RUNNING, _HALTED, _EXHAUSTED = 0, 1, 2
@@ -291,3 +292,46 @@ def collect_histogram(slots) -> dict:
 
 # keep the field tuple importable for bulk consumers
 FIELDS = ALL_FIELDS
+
+
+# --- workloads and the worker-count benchmark (hypervisor.py:355-408) ------------
+
+@dataclass
+class Workload:
+    """Prepared initial configurations of a program batch (hv:355-360).
+    `asts` stays None here: sampling and lowering are out of this engine's
+    scope, programs arrive already lowered."""
+    configs: list
+    asts: list | None
+    aborted: list              # (index, reason) for programs that do not fit memory
+
+
+def build_workload_from_programs(programs, inputs, params: MachineParams) -> Workload:
+    """The packing half of build_workload (hv:362-384) for lowered programs:
+    init_config per program; a CapacityError draw is recorded in `aborted`,
+    never silently dropped (other errors propagate, as in the reference)."""
+    configs, aborted = [], []
+    for k, (prog, x) in enumerate(zip(programs, inputs)):
+        try:
+            configs.append(init_config(prog, x, params))
+        except CapacityError as e:
+            aborted.append((k, str(e)))
+    return Workload(configs=configs, asts=None, aborted=aborted)
+
+
+def throughput_bench(workload: Workload, tau_max: int, workers_list, params: MachineParams,
+                     epoch: int = 64) -> list:
+    """hv:387-408: time the same workload once per entry of `workers_list`;
+    one row {"workers", "wall_time", "vms", "speedup"} each, speedup against
+    the first workers == 1 row (else the first row).  The GPU engine has no
+    worker count: every row runs the whole batch on the device and
+    wall_time is run_batch's device time."""
+    rows = []
+    for w in workers_list:
+        res = run_batch(workload.configs, params, BatchConfig(tau_max=tau_max, epoch=epoch, workers=max(0, int(w)),
+                                                              memory_budget_words=1 << 62))
+        rows.append({"workers": w, "wall_time": res.wall_time, "vms": len(workload.configs), "speedup": 0.0})
+    base = next((r["wall_time"] for r in rows if r["workers"] == 1), rows[0]["wall_time"] if rows else 0.0)
+    for r in rows:
+        r["speedup"] = base / r["wall_time"] if r["wall_time"] > 0 else 0.0
+    return rows

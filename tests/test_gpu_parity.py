@@ -454,3 +454,17 @@ def test_huge_memory_hbm_tiles(pkg, shape):
             if k in FIELDS:
                 got = got.astype(np.uint64)
             np.testing.assert_array_equal(got, want[k], err_msg=f"{shape} tau={tau} {k}")
+
+
+def test_throughput_bench_rows(pkg):
+    """hv:387-408 row format, on the golden busy-beaver programs."""
+    P, H = pkg
+    (g,) = load_family("bb")
+    p = _params(P, g)
+    configs = [P.Config(int(g.c0["iw"][k]), int(g.c0["ac"][k]), tuple(int(v) for v in g.c0["M"][k]),
+                        tuple(int(v) for v in g.c0["u"][k]), tuple(int(v) for v in g.c0["y"][k]))
+               for k in range(g.d)]
+    wl = H.Workload(configs=configs, asts=None, aborted=[])
+    rows = H.throughput_bench(wl, 10 ** 5, [1, 4], p)
+    assert [r["workers"] for r in rows] == [1, 4] and all(r["vms"] == 3 for r in rows)
+    assert rows[0]["speedup"] == 1.0 and all(r["wall_time"] > 0 for r in rows)

@@ -202,3 +202,17 @@ def test_dropin_routes_the_reference_run_batch_without_cpu_fallback():
             RH._worker = original
     finally:
         sys.path.remove(ref)
+
+
+def test_build_workload_from_programs_records_aborted_draws():
+    """hv:362-384: programs too large for memory (or inputs beyond ell) are
+    recorded with their index and reason, the rest become c0."""
+    from paper_2604_12902_b200.hypervisor import Workload, build_workload_from_programs
+    p = MachineParams(w=8, n=8, ell=2, s=2, mu=1)
+    progs = [Program((1, 5, 4, 6)), Program((0,) * 10), Program((7, 2)), Program((1, 1))]
+    inputs = [[], [], [3, 4, 5], [9]]
+    wl = build_workload_from_programs(progs, inputs, p)
+    assert isinstance(wl, Workload) and wl.asts is None
+    assert [k for k, _ in wl.aborted] == [1, 2]
+    assert "memory words" in wl.aborted[0][1] and "ell" in wl.aborted[1][1]
+    assert wl.configs == [init_config(progs[0], [], p), init_config(progs[3], [9], p)]
