@@ -454,6 +454,14 @@ def test_huge_memory_hbm_tiles(pkg, shape):
             if k in FIELDS:
                 got = got.astype(np.uint64)
             np.testing.assert_array_equal(got, want[k], err_msg=f"{shape} tau={tau} {k}")
+        # the fused histogram on HBM tiles (its block copy is the only shared memory there)
+        import torch
+        from paper_2604_12902_b200.engine import DeviceBatch
+        from paper_2604_12902_b200.sharding import histogram_np
+        src = DeviceBatch.from_arrays(c0, p)
+        h = torch.empty(102, dtype=torch.int64, device=src.M.device)
+        H.get_engine(p).run(src, tau, 16, fresh=True, hist=h)
+        np.testing.assert_array_equal(h.cpu().numpy(), histogram_np(want["status"], want["tau_h"]))
 
 
 def test_throughput_bench_rows(pkg):
