@@ -85,6 +85,7 @@ int rasp_run_hist(const rasp_params *p, const rasp_batch *in, const rasp_batch *
     a.g.nm1 = p->n - 1;
     a.g.jm = uint32_t(a.g.mask & uint64_t(p->n - 1));
     a.g.fm = ~0ull / p->n + 1;
+    a.g.m32 = uint32_t((1ull << 32) / p->n);
     a.g.ell = uint32_t(p->ell);
     a.g.s = uint32_t(p->s);
     a.in = side_of(in);
@@ -152,6 +153,7 @@ int rasp_enumerate(const rasp_enum_params *ep, uint64_t first_rank, uint64_t cou
     a.g.nm1 = ep->n - 1;
     a.g.jm = uint32_t(a.g.mask & uint64_t(ep->n - 1));
     a.g.fm = ~0ull / ep->n + 1;
+    a.g.m32 = uint32_t((1ull << 32) / ep->n);
     a.g.ell = 1;
     a.g.s = 1;
     a.first = first_rank;

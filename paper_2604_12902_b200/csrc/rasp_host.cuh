@@ -174,6 +174,7 @@ inline size_t align256(size_t x) { return (x + 255) & ~size_t(255); }
 inline int check_params(const rasp_params *p)
 {
     if (!p || p->w < 1 || p->w > 64 || p->n < 2) return RASP_EPARAM;
+    if (p->n >= (1u << 31)) return RASP_ECAPACITY;   // the kernels' x mod n needs n < 2^31
     const uint64_t limit_m1 = p->w == 64 ? ~0ull : ((1ull << p->w) - 1);
     if (p->ell < 1 || p->s < 1 || p->ell > limit_m1 || p->s > limit_m1) return RASP_EPARAM;
     if (p->ell >= (1ull << 31) || p->s >= (1ull << 31)) return RASP_ECAPACITY;

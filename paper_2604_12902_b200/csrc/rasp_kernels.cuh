@@ -42,13 +42,13 @@ enum class Arith { W1, NARROW, FULL, CELL };
 
 struct Geo {
     uint64_t mask;    // 2^w - 1
-    uint64_t fm;      // ceil(2^64 / n): Lemire fastmod magic (32-bit words, generic n)
+    uint64_t fm;      // ceil(2^64 / n) (unused by the kernels; kept for the layout)
     uint32_t n;
     uint32_t nm1;     // n - 1               (power-of-two n)
     uint32_t jm;      // (2^w - 1) & (n - 1) (power-of-two n)
     uint32_t ell;
     uint32_t s;
-    uint32_t _pad;
+    uint32_t m32;     // floor(2^32 / n): quotient estimate for x mod n of 32-bit words
 };
 
 struct Side {
@@ -176,8 +176,13 @@ __device__ __forceinline__ uint32_t modn(CT x, const Geo &g)
     if constexpr (POW2) {
         return static_cast<uint32_t>(x) & g.nm1;
     } else if constexpr (sizeof(CT) == 4) {
-        const uint64_t low = g.fm * static_cast<uint64_t>(x);
-        return static_cast<uint32_t>(__umul64hi(low, static_cast<uint64_t>(g.n)));
+        // q = floor(x * floor(2^32/n) / 2^32) is floor(x/n) or one less, so
+        // r = x - q*n lies in [0, 2n): one conditional subtract (as an unsigned
+        // min) -- 4 instructions against 8 for a 64-bit Lemire reduction
+        // (n < 2^31, enforced by check_params)
+        const uint32_t xv = static_cast<uint32_t>(x);
+        const uint32_t r = xv - __umulhi(xv, g.m32) * g.n;
+        return min(r, r - g.n);
     } else {
         return static_cast<uint32_t>(x % static_cast<uint64_t>(g.n));
     }
