@@ -629,8 +629,11 @@ __device__ __forceinline__ Fetch<CT> fetch(const LaneState<CT> &L, char *base, u
 #ifndef RASP_LAZY_UD
 #define RASP_LAZY_UD 1
 #endif
+#ifndef RASP_LAZY_UD_BIG
+#define RASP_LAZY_UD_BIG 0
+#endif
 template <bool YG>
-constexpr bool kLazyUd = RASP_LAZY_UD && !YG;
+constexpr bool kLazyUd = RASP_LAZY_UD && (!YG || RASP_LAZY_UD_BIG);
 #ifndef RASP_LAZY_MJ
 #define RASP_LAZY_MJ 0
 #endif
@@ -915,8 +918,7 @@ __device__ __forceinline__ void rasp_step_inc(LaneState<CT> &L, uint32_t &im, ui
         L.ya += q.row;
     }
     const CT i2 = wrap<CT, AR>(L.i + 2, mask);
-    uint32_t im2 = im + 2;
-    im2 = im2 >= g.n ? im2 - g.n : im2;
+    uint32_t im2 = min(im + 2, im + 2 - g.n);             // (im + 2) mod n as one add-min
     im2 = i2 < 2 ? static_cast<uint32_t>(i2) : im2;      // wrapped through 2^w
     const CT ni = selw<CT>(taken, jw, selw<CT>(stay, L.i, i2));
     im = sel32(taken, jn, sel32(stay, im, im2));
