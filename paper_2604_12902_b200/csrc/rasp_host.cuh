@@ -344,10 +344,58 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
     return checked_result(st);
 }
 
+// Per-lane refill for big tiles (refill_kernel): fresh runs whose budget is a
+// positive multiple of the unrolled block, up to kRefillMaxTau steps.  Measured:
+// C5 (tau 1024) 1.84 -> 1.65 ms; the paper row (tau 10^4) 2.60 -> 3.6 ms -- its
+// epochs already keep lanes busy, and a long budget leaves a long tail of
+// warps finishing their last machines.  $RASP_REFILL=0 keeps the epochs, =1
+// uses the refill kernel for any eligible budget (read per run: tests compare
+// both paths in one process).
+constexpr int64_t kRefillMaxTau = 2048;
+inline bool refill_enabled(int64_t tau_max)
+{
+    const char *e = std::getenv("RASP_REFILL");
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    return tau_max <= kRefillMaxTau;
+}
+
+template <class S, class SC, class CT, bool POW2, rasp::Arith AR>
+int launch_refill(const rasp::EpochArgs &base, const Plan &pl, const Device &dv, const Workspace &ws,
+                  uint64_t d, cudaStream_t st)
+{
+    auto kern = rasp::refill_kernel<S, SC, CT, POW2, AR>;
+    LaunchShape sh;
+    const size_t hist_bytes = rasp::kRefillExtra<SC>;   // histogram + parking cells
+    const int rc = launch_shape(reinterpret_cast<const void *>(kern), dv, pl.tile_bytes, hist_bytes, 1, sh);
+    if (rc) return rc;
+    const uint64_t warps = uint64_t(sh.per_sm) * dv.nsm;
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(warps, (d + 31) / 32)));
+    if (std::getenv("RASP_DEBUG"))
+        std::fprintf(stderr, "rasp: refill tile %zu B (%u rows), %d blocks/SM, grid %d\n", pl.tile_bytes,
+                     pl.tile_rows, sh.per_sm, grid);
+    RASP_CUDA(cudaMemsetAsync(ws.sched, 0, sizeof(rasp::Sched), st));
+    rasp::EpochArgs a = base;
+    a.sched = ws.sched;
+    a.count_in = uint32_t(d);
+    a.refill_min = 12;   // C5: 8/12/16 -> 1.655/1.601/1.634 ms (tuning knob RASP_REFILL_MIN)
+    if (const char *e = std::getenv("RASP_REFILL_MIN"))
+        a.refill_min = std::min<uint32_t>(32, std::max<uint32_t>(1, uint32_t(std::strtoul(e, nullptr, 10))));
+    kern<<<grid, 32, pl.tile_bytes + hist_bytes, st>>>(a);
+    RASP_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return checked_result(st);
+}
+
 template <class S, class SC, class CT, bool POW2, rasp::Arith AR>
 int dispatch_budget(const rasp::EpochArgs &a, const Plan &pl, const Device &dv, const Workspace &ws,
                     uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
 {
+    if constexpr (sizeof(SC) >= 4 && AR != rasp::Arith::W1 && AR != rasp::Arith::CELL) {
+        if (pl.big && a.fresh && refill_enabled(tau_max) && tau_max > 0 && tau_max % RASP_UNROLL_BIG == 0 &&
+            tau_max < (int64_t(1) << 31) && d < (uint64_t(1) << 31))
+            return launch_refill<S, SC, CT, POW2, AR>(a, pl, dv, ws, d, st);
+    }
     if (sizeof(SC) >= 4 && pl.big) {
         if (a.fresh) return launch_epochs<S, SC, CT, POW2, AR, false, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);
         return launch_epochs<S, SC, CT, POW2, AR, true, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);

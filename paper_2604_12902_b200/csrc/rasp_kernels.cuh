@@ -160,6 +160,7 @@ struct EpochArgs {
     uint32_t growth;               // next epoch length while machines still halt, x the last one
     uint32_t stable_hi_q8;         // survival ratio (x256) at which the rest runs as one epoch regardless
     unsigned long long *hist;      // int64[102] halting histogram accumulated by the run, or nullptr
+    uint32_t refill_min;           // refill_kernel: free lanes that trigger a refill
 };
 
 template <class CT, Arith AR>
@@ -279,7 +280,42 @@ __device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t nce
     for (; k < ncells; ++k) col[k * 32] = static_cast<SC>(row[k]);
 }
 
-template <class S, class SC>
+// A machine's M row and input tape u[1..ell] in two memory round trips when
+// the tape is short (ell <= 32): the tape's scalar loads ride with the first
+// batch of M's 16-byte loads.  Otherwise load_row twice.
+template <class S, class SC, uint32_t B = 32>
+__device__ __forceinline__ void load_rows_mu(const S *__restrict__ rm, uint32_t n, SC *colm,
+                                             const S *__restrict__ ru, uint32_t ell, SC *colu)
+{
+    constexpr uint32_t PER = 16 / sizeof(S);
+    if (ell > 32 || (reinterpret_cast<uintptr_t>(rm) & 15) != 0 || n < B * PER) {
+        load_row<S, SC, B>(rm, n, colm);
+        load_row<S, SC, B>(ru, ell, colu);
+        return;
+    }
+    check_col_extent(colm, n);
+    check_col_extent(colu, ell);
+    const uint4 *v = reinterpret_cast<const uint4 *>(rm);
+    {
+        uint4 qm[B];
+        S qu[32];
+#pragma unroll
+        for (uint32_t j = 0; j < B; ++j) qm[j] = v[j];
+#pragma unroll
+        for (uint32_t j = 0; j < 32; ++j)
+            if (j < ell) qu[j] = ru[j];
+#pragma unroll
+        for (uint32_t j = 0; j < B; ++j) put16<S, SC>(colm, j * PER, qm[j]);
+#pragma unroll
+        for (uint32_t j = 0; j < 32; ++j)
+            if (j < ell) colu[j * 32] = static_cast<SC>(qu[j]);
+    }
+    load_row<S, SC, B>(rm + B * PER, n - B * PER, colm + B * PER * 32);
+}
+
+// Shared loads in batches of B x 16 B before their global stores (one
+// shared-load latency per batch instead of one per 16 bytes).
+template <class S, class SC, uint32_t B = 8>
 __device__ __forceinline__ void store_row(S *__restrict__ row, uint32_t ncells, const SC *col)
 {
     check_col_extent(col, ncells);
@@ -287,6 +323,13 @@ __device__ __forceinline__ void store_row(S *__restrict__ row, uint32_t ncells, 
     uint32_t k = 0;
     if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
         uint4 *v = reinterpret_cast<uint4 *>(row);
+        for (; k + B * PER <= ncells; k += B * PER) {
+            uint4 q[B];
+#pragma unroll
+            for (uint32_t j = 0; j < B; ++j) q[j] = get16<S, SC>(col, k + j * PER);
+#pragma unroll
+            for (uint32_t j = 0; j < B; ++j) v[k / PER + j] = q[j];
+        }
         for (; k + PER <= ncells; k += PER) v[k / PER] = get16<S, SC>(col, k);
     }
     for (; k < ncells; ++k) row[k] = static_cast<S>(col[k * 32]);
@@ -1286,6 +1329,255 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
             }
         }
     }
+}
+
+// --- per-lane refill for big tiles (fresh runs) ----------------------------------
+//
+// The epoch kernel keeps a tile's 32 machines until the last of them stops or
+// the epoch ends, so a lane whose machine halted early idles: C5's first
+// epoch uses 41% of its lane-steps (p50 halting time 38 against a 320-step
+// epoch; 14% of the machines never halt, so nearly every tile runs it out).
+// For fresh runs whose budget is a multiple of the unrolled block, every
+// machine can start at a block boundary, so its budget also ends on one.
+// After each block of UN steps a lane whose machine stopped moving (halted at
+// its move count, hv:115) or reached tau_max (one more fetch decides fixed or
+// exhausted, as at an epoch end) is finished; its machine stays in place (a
+// fixed point, or parked: opcode 0 stored at its instruction cell, the true
+// value kept in a register).  Once at least `refill_min` lanes are free the
+// warp writes the finished machines back together and hands the free lanes
+// the next machines of its reservation: their rows are copied into the lanes'
+// columns asynchronously (4- or 8-byte cp.async; a TMA box cannot land in a
+// lane column) while the warp steps its other lanes for one more block, and
+// the new machines start at the next block boundary.  A lane whose column is
+// in flight (or that has no machine) steps on two zero cells after the
+// histogram (opcode 0 at i = 0: a fixed point that stores nothing).
+// Reservations are 32 consecutive machine ids claimed with one atomic, one
+// reservation ahead, warmed into L2 when claimed.  One launch runs the whole
+// budget: no epochs, no survivor lists, no reloads.
+// cp.async row fills (4/8-byte copies) for the refill kernel: measured slower
+// (C5 2.06 against 1.65 ms: the copies crowd the steps' shared loads)
+#ifndef RASP_REFILL_ASYNC
+#define RASP_REFILL_ASYNC 0
+#endif
+template <class SC>
+constexpr uint32_t kRefillExtra = 416 + 32 * sizeof(SC) + 16;   // histogram, then the parking cells
+
+__device__ __forceinline__ void cp_async_cell(uint32_t saddr, const void *g, uint32_t bytes)
+{
+    const unsigned long long ga = static_cast<unsigned long long>(__cvta_generic_to_global(g));
+    check_smem(saddr, bytes);
+    if (bytes == 8) asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(saddr), "l"(ga) : "memory");
+    else asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(saddr), "l"(ga) : "memory");
+}
+
+template <class S, class SC, class CT, bool POW2, Arith AR>
+__global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
+{
+    static_assert(sizeof(SC) >= 4 && AR != Arith::W1 && AR != Arith::CELL, "big tiles, w >= 2");
+    constexpr uint32_t UN = RASP_UNROLL_BIG;
+    constexpr uint32_t ROW = 32 * sizeof(SC);
+    constexpr uint32_t SH = sizeof(SC) == 4 ? 7 : 8;   // log2(row bytes)
+    constexpr uint32_t LB = 32;                        // row-load batch (16 B per lane each)
+    // rows copied cell by cell asynchronously when HBM words are tile cells
+    constexpr bool kAsync = RASP_REFILL_ASYNC && sizeof(S) == sizeof(SC);
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const uint32_t lane = threadIdx.x & 31;
+    const Geo g = A.g;
+    const uint32_t n = g.n;
+    char *const tb = reinterpret_cast<char *>(smem_raw);
+    const uint32_t sbase = static_cast<uint32_t>(__cvta_generic_to_shared(smem_raw));
+    const uint32_t lm = sbase + lane * static_cast<uint32_t>(sizeof(SC));
+    char *const gb = reinterpret_cast<char *>(smem_raw) - sbase;
+    const Opq q = {1u, 2u, ROW};
+    const uint32_t U = n * ROW + lm;                    // u[1] of this lane
+    const uint32_t uend = U + g.ell * ROW;
+    const uint32_t yend = g.s * static_cast<uint32_t>(sizeof(S));
+    const uint64_t ucols = static_cast<uint64_t>(g.ell) + 1, ycols = static_cast<uint64_t>(g.s) + 1;
+    const uint32_t d = A.count_in;
+    const uint32_t tau = static_cast<uint32_t>(A.tau_max);
+    const uint32_t rmin = A.refill_min;
+    const uint32_t tile_bytes = A.tile_rows * ROW;
+    uint32_t *const hist_s = reinterpret_cast<uint32_t *>(smem_raw + tile_bytes);
+    const uint32_t P = sbase + tile_bytes + 416;        // parking cells P, P + ROW (zero)
+    if (A.hist)
+        for (uint32_t k = lane; k < 102; k += 32) hist_s[k] = 0;
+    if (lane < 2) *reinterpret_cast<SC *>(gb + P + lane * ROW) = SC(0);
+    __syncwarp();
+    uint32_t *const ctr = &A.sched->tile_ctr[0];
+    const S *const inM = static_cast<const S *>(A.in.M);
+    const S *const inU = static_cast<const S *>(A.in.u);
+    const S *const inY = static_cast<const S *>(A.in.y);
+
+    // a reservation of up to 32 ids [b, b + c); rows warmed into L2
+    auto claim = [&](uint32_t &b, uint32_t &c) {
+        uint32_t x = 0;
+        if (lane == 0) x = atomicAdd(ctr, 32u);
+        x = __shfl_sync(kFull, x, 0);
+        b = x;
+        c = x < d ? min(32u, d - x) : 0u;
+        if (A.pf_dist && lane < c) {
+            const uint64_t id = static_cast<uint64_t>(x) + lane;
+            prefetch_l2(inM + id * n, n * static_cast<uint32_t>(sizeof(S)));
+            prefetch_l2(inU + id * ucols, static_cast<uint32_t>(ucols * sizeof(S)));
+        }
+    };
+
+    LaneState<CT> L;
+    L.i = 0; L.a = 0; L.ua = P; L.ya = 0; L.rem = 0; L.tlast = 0; L.active = false;
+    uint32_t lms = P;          // column the steps read: the lane's own (lm) or the parking cells
+    uint32_t im = 0, ib = 1;   // carried residues of i and i+1 (n not a power of two)
+    uint32_t id = 0;
+    bool has = false;          // the lane holds a machine (not yet written back)
+    bool done = false;         // ... whose verdict is known (it waits for the next refill)
+    bool loading = false;      // ... whose rows are in flight
+    bool halted = false;
+    uint32_t pk = 0;           // parked cell of an exhausted machine (0: none)
+    SC pkv = 0;                // its value
+    CT ni0 = 0, na0 = 0;       // the incoming machine's i, a and cursors
+    uint32_t nua0 = 0, nya0 = 0;
+    char *ybase = nullptr;
+    auto park = [&]() {        // step on the zero cells
+        L.i = 0; L.a = 0; L.ua = P; L.active = false;
+        im = 0; ib = 1;
+        lms = P;
+    };
+    auto start = [&]() {       // the incoming machine takes the lane
+        L.i = ni0; L.a = na0; L.ua = U + nua0 * ROW; L.ya = nya0 * static_cast<uint32_t>(sizeof(S));
+        L.tlast = 0; L.active = true;
+        if constexpr (!POW2) {
+            im = modn<CT, false>(L.i, g);
+            ib = modn<CT, false>(wrap<CT, AR>(L.i + 1, static_cast<CT>(g.mask)), g);
+        }
+        lms = lm;
+        loading = false;
+    };
+    auto load = [&](uint32_t mid) {
+        RASP_CHECK(mid < d, kChkRow, mid, d);
+        const uint64_t m = mid;
+        ni0 = static_cast<CT>(static_cast<const S *>(A.in.iw)[m]);
+        na0 = static_cast<CT>(static_cast<const S *>(A.in.ac)[m]);
+        nua0 = static_cast<uint32_t>(inU[m * ucols]);   // used at start(): the loads stay in flight
+        nya0 = static_cast<uint32_t>(inY[m * ycols]);
+        ybase = reinterpret_cast<char *>(static_cast<S *>(A.out.y) + m * ycols + 1);
+        id = mid;
+        has = true;
+        done = false;
+        if constexpr (kAsync) {
+            park();
+            const S *rm = inM + m * n;
+#pragma unroll 8
+            for (uint32_t k = 0; k < n; ++k) cp_async_cell(lm + k * ROW, rm + k, sizeof(SC));
+            const S *ru = inU + m * ucols + 1;
+#pragma unroll 8
+            for (uint32_t k = 0; k < g.ell; ++k) cp_async_cell(U + k * ROW, ru + k, sizeof(SC));
+            loading = true;
+        } else {
+            load_rows_mu<S, SC, LB>(inM + m * n, n, reinterpret_cast<SC *>(gb + lm), inU + m * ucols + 1, g.ell,
+                                    reinterpret_cast<SC *>(gb + U));
+            start();
+        }
+    };
+    // write the lane's finished machine back (final row, cursors, verdict)
+    auto retire = [&]() {
+        const uint64_t m = id;
+        const uint32_t u0 = (L.ua - U) / ROW;
+        const uint32_t y0 = L.ya / static_cast<uint32_t>(sizeof(S));
+        CT iv = L.i;
+        if constexpr (kRawI<POW2, AR>) iv &= static_cast<CT>(g.mask);
+        static_cast<S *>(A.out.y)[m * ycols] = static_cast<S>(y0);
+        static_cast<S *>(A.out.iw)[m] = static_cast<S>(iv);
+        static_cast<S *>(A.out.ac)[m] = static_cast<S>(L.a);
+        static_cast<S *>(A.out.u)[m * ucols] = static_cast<S>(u0);
+        const int64_t tend = L.tlast;
+        A.out.steps[m] = tend;
+        A.out.status[m] = halted ? kHalted : kExhausted;
+        A.out.tau_h[m] = halted ? tend : -1;
+        if (A.hist) atomicAdd(&hist_s[!halted ? 101u : tend < 100 ? static_cast<uint32_t>(tend) : 100u], 1u);
+        store_row<S, SC>(static_cast<S *>(A.out.M) + m * n, n, reinterpret_cast<const SC *>(gb + lm));
+        // a parked machine: its true cell goes out after the row
+        if (pk) static_cast<S *>(A.out.M)[m * n + ((pk - lm) >> SH)] = static_cast<S>(pkv);
+        pk = 0;
+        has = false;
+        done = false;
+        park();
+    };
+
+    uint32_t r0, n0, r1, n1;
+    claim(r0, n0);
+    claim(r1, n1);
+    bool more = n0 > 0;
+    for (;;) {
+        if constexpr (kAsync) {   // rows issued at the last refill have landed: start those lanes
+            if (__any_sync(kFull, loading)) {
+                asm volatile("cp.async.wait_all;" ::: "memory");
+                if (loading) start();
+            }
+        }
+        // free lanes: no machine, or a finished one (sitting at a fixed point)
+        const bool freel = !has || done;
+        const unsigned freem = __ballot_sync(kFull, freel);
+        const uint32_t nf = __popc(freem);
+        if (nf == 32u || (more && nf >= rmin)) {
+            // write the finished machines back together, then hand the next
+            // machines of the reservations to the free lanes
+            if (done) retire();
+            if (!more) break;   // every lane free and nothing left to hand out
+            const uint32_t rank = __popc(freem & ((1u << lane) - 1u));
+            const uint32_t take = min(nf, n0 + n1);
+            if (freel && rank < take) load(rank < n0 ? r0 + rank : r1 + (rank - n0));
+            if constexpr (kAsync) asm volatile("cp.async.commit_group;" ::: "memory");
+            if (take < n0) {
+                r0 += take;
+                n0 -= take;
+            } else {
+                const uint32_t t1 = take - n0;
+                const bool full = n1 == 32u;
+                r0 = r1 + t1;
+                n0 = n1 - t1;
+                if (full) claim(r1, n1);
+                else n1 = 0;
+                if (n0 == 0 && n1 > 0) {   // the old next reservation is used up too
+                    r0 = r1;
+                    n0 = n1;
+                    if (n1 == 32u) claim(r1, n1);
+                    else n1 = 0;
+                }
+            }
+            more = n0 > 0;
+            asm volatile("" ::: "memory");   // column fills above are visible to the asm loads below
+        }
+        // one block of UN ungated steps; free and loading lanes sit still
+        if constexpr (POW2) {
+#pragma unroll
+            for (uint32_t r = 0; r < UN; ++r)
+                rasp_step_free<SC, CT, POW2, AR, true, true, S>(L, tb, lms, uend, yend, g, q, ybase);
+        } else {
+#pragma unroll
+            for (uint32_t r = 0; r < UN; ++r)
+                rasp_step_inc<SC, CT, AR, true, true, true, S>(L, im, ib, tb, lms, uend, yend, g, q, r, ybase);
+        }
+        // verdicts at the block boundary
+        if (has && !done && !loading) {
+            if (!L.active) {   // stopped moving: halted at its move count
+                done = true;
+                halted = true;
+            } else if (L.tlast >= tau) {   // budget: fixed at tau_max, or exhausted
+                const Fetch<CT> f = fetch<SC, CT, POW2, AR, true>(L, tb, lm, g, q);
+                halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, g, q);
+                done = true;
+                // park it in place: opcode 0 at its instruction cell (the
+                // true value goes out at write-back)
+                pk = ((POW2 ? (static_cast<uint32_t>(L.i) & g.jm) : im) << SH) + lm;
+                pkv = *reinterpret_cast<const SC *>(gb + pk);
+                *reinterpret_cast<SC *>(gb + pk) = SC(0);
+                L.active = false;
+            }
+        }
+    }
+    __syncwarp();
+    if (A.hist)
+        for (uint32_t k = lane; k < 102; k += 32)
+            if (hist_s[k]) atomicAdd(&A.hist[k], static_cast<unsigned long long>(hist_s[k]));
 }
 
 // --- exhaustive enumeration (BASELINE config 4) -------------------

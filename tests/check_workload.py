@@ -16,6 +16,8 @@ Kinds:
           out of place (tile-wise u/y copies) and in place
   big     u32 cells, one-warp BIG tiles with PRI straight to HBM (C5 shape),
           several tiles per warp (the claim loop and the next-tile prefetch)
+  refill  the per-lane refill kernel for fresh big machines (C5 shape; n not a
+          power of two with a tape longer than 32 cells)
   big64   u64 cells (w = 64) BIG tiles, mid-run inputs (per-lane budgets)
   hbm     tiles in HBM (n too large for shared memory)
   enum    the exhaustive-enumeration kernel (config 4 domain, a few programs)
@@ -141,7 +143,12 @@ def main(kind):
     if kind == "mx":
         run_batch_kind(16, 64, 8, 8, 512, 200, 16)
     elif kind == "big":
+        os.environ["RASP_REFILL"] = "0"                     # the epoch kernel's big tiles
         run_batch_kind(32, 256, 32, 32, 1 << 16, 48, 24)   # > 2 tiles per resident warp (888)
+    elif kind == "refill":
+        os.environ["RASP_REFILL"] = "1"                     # the per-lane refill kernel
+        run_batch_kind(32, 256, 32, 32, 1 << 16, 256, 24)  # ~70 machines per resident warp
+        run_batch_kind(32, 250, 40, 16, 20000, 320, 16)    # carried residues, two-pass row loads
     elif kind == "big64":
         run_batch_kind(64, 128, 8, 8, 256, 60, 8, midrun=True)
     elif kind == "hbm":

@@ -11,7 +11,7 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KINDS = ("mx", "big", "big64", "hbm", "enum", "aux")
+KINDS = ("mx", "big", "refill", "big64", "hbm", "enum", "aux")
 
 
 @pytest.fixture(scope="module")
