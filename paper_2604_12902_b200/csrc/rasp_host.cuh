@@ -246,9 +246,33 @@ inline size_t workspace_layout(const rasp_params *p, uint64_t d, const Plan &pl,
     return off;
 }
 
+template <class SC, rasp::Arith AR, bool BUDGET, bool SMEM, bool BIG>
+constexpr bool kRefillOk = sizeof(SC) >= 4 && AR != rasp::Arith::W1 && AR != rasp::Arith::CELL && !BUDGET && SMEM && BIG;
+
+// The refill kernel as the first epoch (big tiles, fresh runs): its launch
+// shape and parameters.  Instantiated only where it applies.
+template <class S, class SC, class CT, bool POW2, rasp::Arith AR>
+int launch_refill_epoch(const rasp::EpochArgs &a, const Plan &pl, const Device &dv, uint64_t d, cudaStream_t st)
+{
+    auto kern = rasp::refill_kernel<S, SC, CT, POW2, AR>;
+    LaunchShape sh;
+    const size_t extra = rasp::kRefillExtra<SC>;   // histogram + parking cells
+    const int rc = launch_shape(reinterpret_cast<const void *>(kern), dv, pl.tile_bytes, extra, 1, sh);
+    if (rc) return rc;
+    const uint64_t warps = uint64_t(sh.per_sm) * dv.nsm;
+    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(warps, (d + 31) / 32)));
+    if (std::getenv("RASP_DEBUG"))
+        std::fprintf(stderr, "rasp: refill epoch K0 %u, tile %zu B (%u rows), %d blocks/SM, grid %d\n", a.K0,
+                     pl.tile_bytes, pl.tile_rows, sh.per_sm, grid);
+    kern<<<grid, 32, pl.tile_bytes + extra, st>>>(a);
+    RASP_CUDA(cudaGetLastError());
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    return RASP_OK;
+}
+
 template <class S, class SC, class CT, bool POW2, rasp::Arith AR, bool BUDGET, bool SMEM, bool BIG = false>
 int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const Workspace &ws,
-                  uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
+                  uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st, bool refill0 = false)
 {
     auto kern = rasp::epoch_kernel<S, SC, CT, POW2, AR, BUDGET, SMEM, BIG>;
     if (SMEM) {
@@ -330,6 +354,20 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
         cudaLaunchAttribute attr[1];
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = 1;
+        if (e == 0 && refill0) {
+            if constexpr (kRefillOk<SC, AR, BUDGET, SMEM, BIG>) {
+                a.refill_min = 12;   // C5: 8/12/16 -> 1.655/1.601/1.634 ms (tuning knob RASP_REFILL_MIN)
+                if (const char *v = std::getenv("RASP_REFILL_MIN"))
+                    a.refill_min = std::min<uint32_t>(32, std::max<uint32_t>(1, uint32_t(std::strtoul(v, nullptr, 10))));
+                // no L2 warm-up of the reservations by default: measured C5 1.606
+                // ms with it, 1.588 without ($RASP_REFILL_PREFETCH=1 turns it on)
+                a.pf_dist = 0;
+                if (const char *v = std::getenv("RASP_REFILL_PREFETCH")) a.pf_dist = uint32_t(std::strtoul(v, nullptr, 10));
+                const int rc = launch_refill_epoch<S, SC, CT, POW2, AR>(a, pl, dv, d, st);
+                if (rc) return rc;
+                continue;
+            }
+        }
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3(unsigned(grid));
         cfg.blockDim = dim3(unsigned(threads));
@@ -344,61 +382,45 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
     return checked_result(st);
 }
 
-// Per-lane refill for big tiles (refill_kernel): fresh runs whose budget is a
-// positive multiple of the unrolled block, up to kRefillMaxTau steps.  Measured:
-// C5 (tau 1024) 1.84 -> 1.65 ms; the paper row (tau 10^4) 2.60 -> 3.6 ms -- its
-// epochs already keep lanes busy, and a long budget leaves a long tail of
-// warps finishing their last machines.  $RASP_REFILL=0 keeps the epochs, =1
-// uses the refill kernel for any eligible budget (read per run: tests compare
-// both paths in one process).
+// Per-lane refill for big tiles (refill_kernel) as the first epoch of fresh
+// runs.  Measured (first-epoch length K0 swept on both paths,
+// scripts/sweep_k0.sh): C5 (tau 1024) 1.84 ms at its best epochs against 1.61
+// with K0 = tau and 1.70-1.78 with K0 = 512/320 plus epochs; the paper row
+// (tau 10^4) 2.60 on epochs against 2.91-3.29 refilled (K0 32..512); paper6
+// (tau 10^6) within 0.3%.  So by default the refill kernel runs only when it
+// can take the whole budget in one launch: tau a multiple of the block and at
+// most kRefillMaxTau.  $RASP_REFILL=0 keeps the epochs; =1 runs the refill
+// kernel as the first epoch of any fresh big-tile run, K0 = the first-epoch
+// length rounded up to the block (survivors continue on the epoch kernel).
+// Read per run: tests compare the paths in one process.
 constexpr int64_t kRefillMaxTau = 2048;
-inline bool refill_enabled(int64_t tau_max)
+inline int refill_mode()
 {
     const char *e = std::getenv("RASP_REFILL");
-    if (e && e[0] == '0') return false;
-    if (e && e[0] == '1') return true;
-    return tau_max <= kRefillMaxTau;
-}
-
-template <class S, class SC, class CT, bool POW2, rasp::Arith AR>
-int launch_refill(const rasp::EpochArgs &base, const Plan &pl, const Device &dv, const Workspace &ws,
-                  uint64_t d, cudaStream_t st)
-{
-    auto kern = rasp::refill_kernel<S, SC, CT, POW2, AR>;
-    LaunchShape sh;
-    const size_t hist_bytes = rasp::kRefillExtra<SC>;   // histogram + parking cells
-    const int rc = launch_shape(reinterpret_cast<const void *>(kern), dv, pl.tile_bytes, hist_bytes, 1, sh);
-    if (rc) return rc;
-    const uint64_t warps = uint64_t(sh.per_sm) * dv.nsm;
-    const int grid = int(std::max<uint64_t>(1, std::min<uint64_t>(warps, (d + 31) / 32)));
-    if (std::getenv("RASP_DEBUG"))
-        std::fprintf(stderr, "rasp: refill tile %zu B (%u rows), %d blocks/SM, grid %d\n", pl.tile_bytes,
-                     pl.tile_rows, sh.per_sm, grid);
-    RASP_CUDA(cudaMemsetAsync(ws.sched, 0, sizeof(rasp::Sched), st));
-    rasp::EpochArgs a = base;
-    a.sched = ws.sched;
-    a.count_in = uint32_t(d);
-    // no L2 warm-up of the reservations by default: measured C5 1.606 ms with it,
-    // 1.588 without (the rows are read once; $RASP_REFILL_PREFETCH=1 turns it on)
-    a.pf_dist = 0;
-    if (const char *e = std::getenv("RASP_REFILL_PREFETCH")) a.pf_dist = uint32_t(std::strtoul(e, nullptr, 10));
-    a.refill_min = 12;   // C5: 8/12/16 -> 1.655/1.601/1.634 ms (tuning knob RASP_REFILL_MIN)
-    if (const char *e = std::getenv("RASP_REFILL_MIN"))
-        a.refill_min = std::min<uint32_t>(32, std::max<uint32_t>(1, uint32_t(std::strtoul(e, nullptr, 10))));
-    kern<<<grid, 32, pl.tile_bytes + hist_bytes, st>>>(a);
-    RASP_CUDA(cudaGetLastError());
-    g_launches.fetch_add(1, std::memory_order_relaxed);
-    return checked_result(st);
+    if (e && e[0] == '0') return 0;
+    if (e && e[0] == '1') return 1;
+    return 2;   // auto
 }
 
 template <class S, class SC, class CT, bool POW2, rasp::Arith AR>
 int dispatch_budget(const rasp::EpochArgs &a, const Plan &pl, const Device &dv, const Workspace &ws,
                     uint64_t d, int64_t tau_max, int64_t epoch, cudaStream_t st)
 {
-    if constexpr (sizeof(SC) >= 4 && AR != rasp::Arith::W1 && AR != rasp::Arith::CELL) {
-        if (pl.big && a.fresh && refill_enabled(tau_max) && tau_max > 0 && tau_max % RASP_UNROLL_BIG == 0 &&
-            tau_max < (int64_t(1) << 31) && d < (uint64_t(1) << 31))
-            return launch_refill<S, SC, CT, POW2, AR>(a, pl, dv, ws, d, st);
+    if constexpr (kRefillOk<SC, AR, false, true, true>) {
+        // the refill kernel runs the first epoch: K0 = the first-epoch length
+        // rounded up to the unrolled block, or the whole budget when that
+        // covers it and is a multiple of the block (else a block less)
+        constexpr int64_t UN = RASP_UNROLL_BIG;
+        const int mode = refill_mode();
+        int64_t k0 = 0;
+        if (mode == 2 && tau_max % UN == 0 && tau_max <= kRefillMaxTau) k0 = tau_max;
+        if (mode == 1) {
+            k0 = (std::max<int64_t>(epoch, 1) + UN - 1) / UN * UN;
+            if (k0 >= tau_max) k0 = tau_max / UN * UN;
+        }
+        if (pl.big && a.fresh && k0 >= UN && k0 <= int64_t(max_epoch_len()) && k0 < (int64_t(1) << 31) &&
+            d < (uint64_t(1) << 31))
+            return launch_epochs<S, SC, CT, POW2, AR, false, true, true>(a, pl, dv, ws, d, tau_max, k0, st, true);
     }
     if (sizeof(SC) >= 4 && pl.big) {
         if (a.fresh) return launch_epochs<S, SC, CT, POW2, AR, false, true, true>(a, pl, dv, ws, d, tau_max, epoch, st);

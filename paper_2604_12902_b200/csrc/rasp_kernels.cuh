@@ -976,6 +976,50 @@ __device__ __forceinline__ void rasp_step_inc(LaneState<CT> &L, uint32_t &im, ui
     L.i = ni;
 }
 
+// The last block of epoch e to finish plans epoch e + 1 (K[e+1], covered[e+1])
+// from the survival ratio of this epoch.  Called by one thread per block.
+__device__ __forceinline__ void plan_next_epoch(const EpochArgs &A, uint32_t count, uint32_t K, int64_t covered,
+                                                uint32_t ntiles)
+{
+    Sched *sc = A.sched;
+    const uint32_t e = A.e;
+    __threadfence();
+    if (atomicAdd(&sc->blocks_done[e], 1u) == gridDim.x - 1) {
+        __threadfence();
+        const uint32_t cout = atomicAdd(&sc->count[e], 0u);
+        const int64_t cov = covered + K;
+        const int64_t left = A.tau_max - cov;
+        uint32_t kn = 0;
+        if (cout > 0 && left > 0 && ntiles > 0) {
+            // the rest of the budget runs as one epoch once the live set has
+            // stopped halting: at least stable_q8/256 of it survived this
+            // epoch and the rest is at most `jump` times this epoch, or
+            // stable_hi_q8/256 of it survived (a long budget jumped to while
+            // machines still halt leaves their lanes idle for all of it);
+            // otherwise keep compacting at 2x length
+            const uint64_t surv = 256ull * cout;
+            const bool stable =
+                (surv >= static_cast<uint64_t>(A.stable_q8) * count &&
+                 static_cast<uint64_t>(left) <= static_cast<uint64_t>(A.jump) * (K > 0 ? K : 1u)) ||
+                surv >= static_cast<uint64_t>(A.stable_hi_q8) * count;
+            uint64_t want = stable ? static_cast<uint64_t>(left)
+                                   : static_cast<uint64_t>(A.growth) * (K > 0 ? K : 1u);
+            // never leave a sliver of the budget (under a quarter of this
+            // epoch) for one more epoch: it would reload every survivor
+            // for a few steps (C5 at first epoch 336: 336, 672, 16)
+            if (static_cast<uint64_t>(left) > want &&
+                static_cast<uint64_t>(left) - want < (want >> 2))
+                want = static_cast<uint64_t>(left);
+            kn = static_cast<uint32_t>(min(min(want, static_cast<uint64_t>(left)),
+                                           static_cast<uint64_t>(A.kmax)));
+        }
+        if (e + 1 < kMaxEpochs) {
+            sc->K[e + 1] = kn;
+            sc->covered[e + 1] = cov;
+        }
+    }
+}
+
 template <class S, class SC, class CT, bool POW2, Arith AR, bool BUDGET, bool SMEM, bool BIG = false>
 __global__ void __launch_bounds__(BIG ? 32 : 32 * RASP_BLOCK_WARPS, BIG ? 8 : (SMEM ? RASP_MIN_BLOCKS : 1))
 epoch_kernel(const EpochArgs A, SC *gtiles)
@@ -1293,43 +1337,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
     if (A.hist)
         for (uint32_t k = threadIdx.x; k < 102; k += blockDim.x)
             if (hist_s[k]) atomicAdd(&A.hist[k], static_cast<unsigned long long>(hist_s[k]));
-    if (threadIdx.x == 0) {
-        __threadfence();
-        if (atomicAdd(&sc->blocks_done[e], 1u) == gridDim.x - 1) {
-            __threadfence();
-            const uint32_t cout = atomicAdd(&sc->count[e], 0u);
-            const int64_t cov = covered + K;
-            const int64_t left = A.tau_max - cov;
-            uint32_t kn = 0;
-            if (cout > 0 && left > 0 && ntiles > 0) {
-                // the rest of the budget runs as one epoch once the live set has
-                // stopped halting: at least stable_q8/256 of it survived this
-                // epoch and the rest is at most `jump` times this epoch, or
-                // stable_hi_q8/256 of it survived (a long budget jumped to while
-                // machines still halt leaves their lanes idle for all of it);
-                // otherwise keep compacting at 2x length
-                const uint64_t surv = 256ull * cout;
-                const bool stable =
-                    (surv >= static_cast<uint64_t>(A.stable_q8) * count &&
-                     static_cast<uint64_t>(left) <= static_cast<uint64_t>(A.jump) * (K > 0 ? K : 1u)) ||
-                    surv >= static_cast<uint64_t>(A.stable_hi_q8) * count;
-                uint64_t want = stable ? static_cast<uint64_t>(left)
-                                       : static_cast<uint64_t>(A.growth) * (K > 0 ? K : 1u);
-                // never leave a sliver of the budget (under a quarter of this
-                // epoch) for one more epoch: it would reload every survivor
-                // for a few steps (C5 at first epoch 336: 336, 672, 16)
-                if (static_cast<uint64_t>(left) > want &&
-                    static_cast<uint64_t>(left) - want < (want >> 2))
-                    want = static_cast<uint64_t>(left);
-                kn = static_cast<uint32_t>(min(min(want, static_cast<uint64_t>(left)),
-                                               static_cast<uint64_t>(A.kmax)));
-            }
-            if (e + 1 < kMaxEpochs) {
-                sc->K[e + 1] = kn;
-                sc->covered[e + 1] = cov;
-            }
-        }
-    }
+    if (threadIdx.x == 0) plan_next_epoch(A, count, K, covered, ntiles);
 }
 
 // --- per-lane refill for big tiles (fresh runs) ----------------------------------
@@ -1340,9 +1348,11 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
 // epoch; 14% of the machines never halt, so nearly every tile runs it out).
 // For fresh runs whose budget is a multiple of the unrolled block, every
 // machine can start at a block boundary, so its budget also ends on one.
-// After each block of UN steps a lane whose machine stopped moving (halted at
-// its move count, hv:115) or reached tau_max (one more fetch decides fixed or
-// exhausted, as at an epoch end) is finished; its machine stays in place (a
+// The kernel runs the first epoch of K0 steps (a multiple of the block): after
+// each block of UN steps a lane whose machine stopped moving (halted at its
+// move count, hv:115) or reached K0 (one more fetch decides: fixed there,
+// exhausted at K0 = tau_max, else a survivor for the epoch kernel's later
+// epochs, appended to the survivor list like theirs) is finished; its machine stays in place (a
 // fixed point, or parked: opcode 0 stored at its instruction cell, the true
 // value kept in a register).  Once at least `refill_min` lanes are free the
 // warp writes the finished machines back together and hands the free lanes
@@ -1353,8 +1363,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
 // in flight (or that has no machine) steps on two zero cells after the
 // histogram (opcode 0 at i = 0: a fixed point that stores nothing).
 // Reservations are 32 consecutive machine ids claimed with one atomic, one
-// reservation ahead, warmed into L2 when claimed.  One launch runs the whole
-// budget: no epochs, no survivor lists, no reloads.
+// reservation ahead.  With K0 = tau_max one launch runs the whole budget.
 // cp.async row fills (4/8-byte copies) for the refill kernel: measured slower
 // (C5 2.06 against 1.65 ms: the copies crowd the steps' shared loads)
 #ifndef RASP_REFILL_ASYNC
@@ -1395,7 +1404,8 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
     const uint32_t yend = g.s * static_cast<uint32_t>(sizeof(S));
     const uint64_t ucols = static_cast<uint64_t>(g.ell) + 1, ycols = static_cast<uint64_t>(g.s) + 1;
     const uint32_t d = A.count_in;
-    const uint32_t tau = static_cast<uint32_t>(A.tau_max);
+    const uint32_t K = A.K0;                                 // this epoch: a multiple of UN, <= tau_max
+    const bool last = static_cast<int64_t>(K) >= A.tau_max;   // K0 covers the budget
     const uint32_t rmin = A.refill_min;
     const uint32_t tile_bytes = A.tile_rows * ROW;
     uint32_t *const hist_s = reinterpret_cast<uint32_t *>(smem_raw + tile_bytes);
@@ -1432,6 +1442,7 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
     bool done = false;         // ... whose verdict is known (it waits for the next refill)
     bool loading = false;      // ... whose rows are in flight
     bool halted = false;
+    bool surv = false;         // ... that survives this epoch (reached K0 < tau_max, not fixed)
     uint32_t pk = 0;           // parked cell of an exhausted machine (0: none)
     SC pkv = 0;                // its value
     CT ni0 = 0, na0 = 0;       // the incoming machine's i, a and cursors
@@ -1463,6 +1474,7 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
         id = mid;
         has = true;
         done = false;
+        surv = false;
         if constexpr (kAsync) {
             park();
             const S *rm = inM + m * n;
@@ -1489,11 +1501,13 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
         static_cast<S *>(A.out.iw)[m] = static_cast<S>(iv);
         static_cast<S *>(A.out.ac)[m] = static_cast<S>(L.a);
         static_cast<S *>(A.out.u)[m * ucols] = static_cast<S>(u0);
-        const int64_t tend = L.tlast;
-        A.out.steps[m] = tend;
-        A.out.status[m] = halted ? kHalted : kExhausted;
-        A.out.tau_h[m] = halted ? tend : -1;
-        if (A.hist) atomicAdd(&hist_s[!halted ? 101u : tend < 100 ? static_cast<uint32_t>(tend) : 100u], 1u);
+        if (!surv) {   // a survivor's verdict fields are written by the epoch it finishes in
+            const int64_t tend = L.tlast;
+            A.out.steps[m] = tend;
+            A.out.status[m] = halted ? kHalted : kExhausted;
+            A.out.tau_h[m] = halted ? tend : -1;
+            if (A.hist) atomicAdd(&hist_s[!halted ? 101u : tend < 100 ? static_cast<uint32_t>(tend) : 100u], 1u);
+        }
         store_row<S, SC, 8>(static_cast<S *>(A.out.M) + m * n, n, reinterpret_cast<const SC *>(gb + lm));
         // a parked machine: its true cell goes out after the row
         if (pk) static_cast<S *>(A.out.M)[m * n + ((pk - lm) >> SH)] = static_cast<S>(pkv);
@@ -1519,8 +1533,20 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
         const unsigned freem = __ballot_sync(kFull, freel);
         const uint32_t nf = __popc(freem);
         if (nf == 32u || (more && nf >= rmin)) {
-            // write the finished machines back together, then hand the next
-            // machines of the reservations to the free lanes
+            // write the finished machines back together (survivors onto the
+            // next epoch's list), then hand the next machines of the
+            // reservations to the free lanes
+            const unsigned sv = __ballot_sync(kFull, done && surv);
+            if (sv) {
+                uint32_t sb = 0;
+                if (lane == 0) sb = atomicAdd(&A.sched->count[0], static_cast<uint32_t>(__popc(sv)));
+                sb = __shfl_sync(kFull, sb, 0);
+                if (done && surv) {
+                    const uint32_t slot = sb + __popc(sv & ((1u << lane) - 1u));
+                    RASP_CHECK(slot < d, kChkList, slot, d);
+                    A.list_out[slot] = id;
+                }
+            }
             if (done) retire();
             if (!more) break;   // every lane free and nothing left to hand out
             const uint32_t rank = __popc(freem & ((1u << lane) - 1u));
@@ -1562,9 +1588,10 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
             if (!L.active) {   // stopped moving: halted at its move count
                 done = true;
                 halted = true;
-            } else if (L.tlast >= tau) {   // budget: fixed at tau_max, or exhausted
+            } else if (L.tlast >= K) {   // epoch end: fixed at K0, exhausted, or a survivor
                 const Fetch<CT> f = fetch<SC, CT, POW2, AR, true>(L, tb, lm, g, q);
                 halted = is_fixed<CT, POW2, AR>(L, f, uend, yend, g, q);
+                surv = !halted && !last;
                 done = true;
                 // park it in place: opcode 0 at its instruction cell (the
                 // true value goes out at write-back)
@@ -1579,6 +1606,7 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
     if (A.hist)
         for (uint32_t k = lane; k < 102; k += 32)
             if (hist_s[k]) atomicAdd(&A.hist[k], static_cast<unsigned long long>(hist_s[k]));
+    if (lane == 0) plan_next_epoch(A, d, K, 0, (d + 31) / 32);
 }
 
 // --- exhaustive enumeration (BASELINE config 4) -------------------

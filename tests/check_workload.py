@@ -147,8 +147,9 @@ def main(kind):
         run_batch_kind(32, 256, 32, 32, 1 << 16, 48, 24)   # > 2 tiles per resident warp (888)
     elif kind == "refill":
         os.environ["RASP_REFILL"] = "1"                     # the per-lane refill kernel
-        run_batch_kind(32, 256, 32, 32, 1 << 16, 256, 24)  # ~70 machines per resident warp
-        run_batch_kind(32, 250, 40, 16, 20000, 320, 16)    # carried residues, two-pass row loads
+        run_batch_kind(32, 256, 32, 32, 1 << 16, 256, 256)  # whole budget, ~70 machines per resident warp
+        run_batch_kind(32, 256, 32, 32, 20000, 256, 24)     # first epoch of 32, survivors on epochs
+        run_batch_kind(32, 250, 40, 16, 20000, 320, 16)     # carried residues, two-pass row loads
     elif kind == "big64":
         run_batch_kind(64, 128, 8, 8, 256, 60, 8, midrun=True)
     elif kind == "hbm":

@@ -65,7 +65,7 @@ def _oracle(c0, p, tau):
     return want
 
 
-def _run(torch, p, c0, tau, word, inplace, refill, rmin=None):
+def _run(torch, p, c0, tau, word, inplace, refill, rmin=None, epoch=None):
     from paper_2604_12902_b200 import _native
     from paper_2604_12902_b200.engine import DeviceBatch
     from paper_2604_12902_b200.hypervisor import get_engine
@@ -86,7 +86,7 @@ def _run(torch, p, c0, tau, word, inplace, refill, rmin=None):
         eng.warm(wb, True)
         torch.cuda.synchronize()
         n0 = _native.load().rasp_launch_count()
-        eng.run(src, tau, 16, out=None if inplace else dst, fresh=True, hist=hist)
+        eng.run(src, tau, epoch or max(tau, 1), out=None if inplace else dst, fresh=True, hist=hist)
         torch.cuda.synchronize()
         launches = _native.load().rasp_launch_count() - n0
     finally:
@@ -130,16 +130,42 @@ def test_refill_matches_oracle_and_epochs(torch_mod, case):
         g = got[f].astype(np.uint64) if f in FIELDS else got[f]
         np.testing.assert_array_equal(g, want[f], err_msg=f"{case} field {f}")
     np.testing.assert_array_equal(hist, _hist_of(want))
-    epo, hist_e, launches_e = _run(torch, p, c0, tau, word, inplace, False)
+    epo, hist_e, launches_e = _run(torch, p, c0, tau, word, inplace, False, epoch=16)
     assert launches_e > launches or tau <= 16
     for f in RESULTS:
         np.testing.assert_array_equal(epo[f], got[f], err_msg=f"{case} field {f} (epoch path)")
     np.testing.assert_array_equal(hist_e, hist)
 
 
+# w, n, ell, s, d, tau, first epoch, word dtype, in place
+SURVIVOR_CASES = [
+    (32, 256, 32, 32, 20000, 1000, 48, np.uint32, False),    # budget not a multiple of the block
+    (32, 250, 40, 16, 8000, 3000, 320, np.uint32, True),     # carried residues, two-pass loads
+    (64, 128, 8, 8, 4000, 700, 100, np.uint64, False),       # u64 cells; K0 = 112
+]
+
+
+@pytest.mark.parametrize("case", SURVIVOR_CASES, ids=lambda c: f"w{c[0]}n{c[1]}t{c[5]}k{c[6]}")
+def test_refill_first_epoch_with_survivors(torch_mod, case):
+    """$RASP_REFILL=1: the refill kernel runs the first epoch (K0 = the first-epoch
+    length rounded up to the block) and appends the machines still running
+    to the survivor list; the epoch kernel runs the rest of the budget."""
+    torch = torch_mod
+    w, n, ell, s, d, tau, epoch, word, inplace = case
+    p, c0 = _inputs((w, n, ell, s, d), seed=n + tau)
+    want = _oracle(c0, p, tau)
+    got, hist, launches = _run(torch, p, c0, tau, word, inplace, True, epoch=epoch)
+    assert launches > (1 if inplace else 3), launches   # survivors continued on later epochs
+    for f in RESULTS:
+        g = got[f].astype(np.uint64) if f in FIELDS else got[f]
+        np.testing.assert_array_equal(g, want[f], err_msg=f"{case} field {f}")
+    np.testing.assert_array_equal(hist, _hist_of(want))
+
+
 def test_refill_not_used_where_it_loses(torch_mod):
-    """Auto mode keeps the epochs for long budgets (tau > 2048: the paper row
-    measured 2.60 ms on epochs against 3.6 ms refilled) and for mid-run inputs."""
+    """Auto mode runs the refill kernel only when it takes the whole budget in
+    one launch (tau a multiple of the block, at most 2048); longer budgets
+    keep the epochs (the paper row: 2.60 ms on epochs, 2.91+ refilled)."""
     torch = torch_mod
     case = (32, 256, 32, 32, 3000, 4096, np.uint32, True, None)
     p, c0 = _inputs(case, seed=7)
