@@ -253,22 +253,38 @@ __device__ __forceinline__ void check_col_extent(const SC *col, uint32_t ncells)
 #endif
 }
 
+// Rows that do not start on a 16-byte boundary (machine m's row starts at
+// m * n words: with n * sizeof(S) not a multiple of 16, every other row is
+// misaligned -- the paper rows' n = 250) take a scalar head up to the
+// boundary, loaded together with the first vector batch and stored after the
+// vector part, so a row still costs ceil(cells / (16 B x B)) memory round
+// trips instead of one per B scalars.
 template <class S, class SC, uint32_t B = 8>
 __device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t ncells, SC *col)
 {
     check_col_extent(col, ncells);
     constexpr uint32_t PER = 16 / sizeof(S);
     uint32_t k = 0;
-    if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
-        const uint4 *v = reinterpret_cast<const uint4 *>(row);
+    const uintptr_t ra = reinterpret_cast<uintptr_t>(row);
+    if (ra % sizeof(S) == 0) {
+        const uint32_t head = min(static_cast<uint32_t>(((16 - (ra & 15)) & 15) / sizeof(S)), ncells);
+        S h[PER > 1 ? PER - 1 : 1];
+#pragma unroll
+        for (uint32_t j = 0; j + 1 < PER; ++j)
+            if (j < head) h[j] = row[j];
+        k = head;
+        const uint4 *v = reinterpret_cast<const uint4 *>(row + head);
         for (; k + B * PER <= ncells; k += B * PER) {
             uint4 q[B];
 #pragma unroll
-            for (uint32_t j = 0; j < B; ++j) q[j] = v[k / PER + j];
+            for (uint32_t j = 0; j < B; ++j) q[j] = v[(k - head) / PER + j];
 #pragma unroll
             for (uint32_t j = 0; j < B; ++j) put16<S, SC>(col, k + j * PER, q[j]);
         }
-        for (; k + PER <= ncells; k += PER) put16<S, SC>(col, k, v[k / PER]);
+        for (; k + PER <= ncells; k += PER) put16<S, SC>(col, k, v[(k - head) / PER]);
+#pragma unroll
+        for (uint32_t j = 0; j + 1 < PER; ++j)
+            if (j < head) col[j * 32] = static_cast<SC>(h[j]);
     }
     for (; k + B <= ncells; k += B) {
         S e[B];
@@ -322,16 +338,19 @@ __device__ __forceinline__ void store_row(S *__restrict__ row, uint32_t ncells, 
     check_col_extent(col, ncells);
     constexpr uint32_t PER = 16 / sizeof(S);
     uint32_t k = 0;
-    if ((reinterpret_cast<uintptr_t>(row) & 15) == 0) {
-        uint4 *v = reinterpret_cast<uint4 *>(row);
+    const uintptr_t ra = reinterpret_cast<uintptr_t>(row);
+    if (ra % sizeof(S) == 0) {   // scalar head up to the 16-byte boundary, then vectors
+        const uint32_t head = min(static_cast<uint32_t>(((16 - (ra & 15)) & 15) / sizeof(S)), ncells);
+        for (; k < head; ++k) row[k] = static_cast<S>(col[k * 32]);
+        uint4 *v = reinterpret_cast<uint4 *>(row + head);
         for (; k + B * PER <= ncells; k += B * PER) {
             uint4 q[B];
 #pragma unroll
             for (uint32_t j = 0; j < B; ++j) q[j] = get16<S, SC>(col, k + j * PER);
 #pragma unroll
-            for (uint32_t j = 0; j < B; ++j) v[k / PER + j] = q[j];
+            for (uint32_t j = 0; j < B; ++j) v[(k - head) / PER + j] = q[j];
         }
-        for (; k + PER <= ncells; k += PER) v[k / PER] = get16<S, SC>(col, k);
+        for (; k + PER <= ncells; k += PER) v[(k - head) / PER] = get16<S, SC>(col, k);
     }
     for (; k < ncells; ++k) row[k] = static_cast<S>(col[k * 32]);
 }
