@@ -297,10 +297,52 @@ __device__ __forceinline__ void load_row(const S *__restrict__ row, uint32_t nce
 }
 
 // A machine's M row and input tape u[1..ell] in two memory round trips when
-// the tape is short (ell <= 32): the tape's scalar loads ride with the first
-// batch of M's 16-byte loads.  Otherwise load_row twice.
+// the tape is short (ell <= 32): the tape's scalar loads (and a misaligned
+// row's scalar head) ride with the first batch of M's 16-byte loads.
+// Otherwise load_row twice.
 template <class S, class SC, uint32_t B = 32>
 __device__ __forceinline__ void load_rows_mu(const S *__restrict__ rm, uint32_t n, SC *colm,
+                                             const S *__restrict__ ru, uint32_t ell, SC *colu)
+{
+    constexpr uint32_t PER = 16 / sizeof(S);
+    const uintptr_t ra = reinterpret_cast<uintptr_t>(rm);
+    const uint32_t head = static_cast<uint32_t>(((16 - (ra & 15)) & 15) / sizeof(S));
+    if (ell > 32 || ra % sizeof(S) != 0 || n < head + B * PER) {
+        load_row<S, SC, B>(rm, n, colm);
+        load_row<S, SC, B>(ru, ell, colu);
+        return;
+    }
+    check_col_extent(colm, n);
+    check_col_extent(colu, ell);
+    const uint4 *v = reinterpret_cast<const uint4 *>(rm + head);
+    {
+        S h[PER > 1 ? PER - 1 : 1];
+        uint4 qm[B];
+        S qu[32];
+#pragma unroll
+        for (uint32_t j = 0; j + 1 < PER; ++j)
+            if (j < head) h[j] = rm[j];
+#pragma unroll
+        for (uint32_t j = 0; j < B; ++j) qm[j] = v[j];
+#pragma unroll
+        for (uint32_t j = 0; j < 32; ++j)
+            if (j < ell) qu[j] = ru[j];
+#pragma unroll
+        for (uint32_t j = 0; j < B; ++j) put16<S, SC>(colm, head + j * PER, qm[j]);
+#pragma unroll
+        for (uint32_t j = 0; j < 32; ++j)
+            if (j < ell) colu[j * 32] = static_cast<SC>(qu[j]);
+#pragma unroll
+        for (uint32_t j = 0; j + 1 < PER; ++j)
+            if (j < head) colm[j * 32] = static_cast<SC>(h[j]);
+    }
+    load_row<S, SC, B>(rm + head + B * PER, n - head - B * PER, colm + (head + B * PER) * 32);
+}
+
+// The same for 16-byte aligned M rows only (the refill kernel: the general
+// form's registers measured +1.2% on C5, whose rows are aligned).
+template <class S, class SC, uint32_t B = 32>
+__device__ __forceinline__ void load_rows_mu_aligned(const S *__restrict__ rm, uint32_t n, SC *colm,
                                              const S *__restrict__ ru, uint32_t ell, SC *colu)
 {
     constexpr uint32_t PER = 16 / sizeof(S);
@@ -1183,7 +1225,10 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 L.ua = U + static_cast<uint32_t>(srcU[0]) * ROW;
                 L.ya = Y + static_cast<uint32_t>(srcY[0]) * YSTEP;
                 if constexpr (BIG) ybase = reinterpret_cast<char *>(static_cast<S *>(A.out.y) + id * ycols + 1);
-                if constexpr (!MX) {
+                if constexpr (BIG) {
+                    load_rows_mu<S, SC, LB>(srcM, n, reinterpret_cast<SC *>(gb + lm), srcU + 1, A.g.ell,
+                                            reinterpret_cast<SC *>(gb + U));
+                } else if constexpr (!MX) {
                     load_row<S, SC, LB>(srcM, n, reinterpret_cast<SC *>(gb + lm));
                     load_row<S, SC, LB>(srcU + 1, A.g.ell, reinterpret_cast<SC *>(gb + U));
                 }
@@ -1504,8 +1549,8 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
             for (uint32_t k = 0; k < g.ell; ++k) cp_async_cell(U + k * ROW, ru + k, sizeof(SC));
             loading = true;
         } else {
-            load_rows_mu<S, SC, LB>(inM + m * n, n, reinterpret_cast<SC *>(gb + lm), inU + m * ucols + 1, g.ell,
-                                    reinterpret_cast<SC *>(gb + U));
+            load_rows_mu_aligned<S, SC, LB>(inM + m * n, n, reinterpret_cast<SC *>(gb + lm), inU + m * ucols + 1,
+                                            g.ell, reinterpret_cast<SC *>(gb + U));
             start();
         }
     };
