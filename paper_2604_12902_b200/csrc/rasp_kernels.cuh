@@ -1427,7 +1427,8 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
 // in flight (or that has no machine) steps on two zero cells after the
 // histogram (opcode 0 at i = 0: a fixed point that stores nothing).
 // Reservations are 32 consecutive machine ids claimed with one atomic, one
-// reservation ahead.  With K0 = tau_max one launch runs the whole budget.
+// reservation ahead; each refill warms L2 with the rows of the next pf_dist
+// ids.  With K0 = tau_max one launch runs the whole budget.
 // cp.async row fills (4/8-byte copies) for the refill kernel: measured slower
 // (C5 2.06 against 1.65 ms: the copies crowd the steps' shared loads)
 #ifndef RASP_REFILL_ASYNC
@@ -1490,7 +1491,7 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
         x = __shfl_sync(kFull, x, 0);
         b = x;
         c = x < d ? min(32u, d - x) : 0u;
-        if (A.pf_dist && lane < c) {
+        if (A.pf_dist == 1 && lane < c) {
             const uint64_t id = static_cast<uint64_t>(x) + lane;
             prefetch_l2(inM + id * n, n * static_cast<uint32_t>(sizeof(S)));
             prefetch_l2(inU + id * ucols, static_cast<uint32_t>(ucols * sizeof(S)));
@@ -1635,6 +1636,14 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
                 }
             }
             more = n0 > 0;
+            if (A.pf_dist >= 2) {   // warm L2 with the pf_dist machines the next refills will take
+                const uint32_t nx = min(n0 + n1, min(A.pf_dist, 32u));
+                if (lane < nx) {
+                    const uint64_t id = lane < n0 ? r0 + lane : r1 + (lane - n0);
+                    prefetch_l2(inM + id * n, n * static_cast<uint32_t>(sizeof(S)));
+                    prefetch_l2(inU + id * ucols, static_cast<uint32_t>(ucols * sizeof(S)));
+                }
+            }
             asm volatile("" ::: "memory");   // column fills above are visible to the asm loads below
         }
         // one block of UN ungated steps; free and loading lanes sit still
