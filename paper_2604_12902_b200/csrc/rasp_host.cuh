@@ -390,7 +390,7 @@ int launch_epochs(const rasp::EpochArgs &base, Plan pl, const Device &dv, const 
 // (tau 10^4) 2.60 on epochs against 2.91-3.29 refilled (K0 32..512); paper6
 // (tau 10^6) within 0.3%.  So by default the refill kernel runs only when it
 // can take the whole budget in one launch: tau a multiple of the block and at
-// most kRefillMaxTau.  $RASP_REFILL=0 keeps the epochs; =1 runs the refill
+// most kRefillMaxTau, and the machine rows 16-byte aligned.  $RASP_REFILL=0 keeps the epochs; =1 runs the refill
 // kernel as the first epoch of any fresh big-tile run, K0 = the first-epoch
 // length rounded up to the block (survivors continue on the epoch kernel).
 // Read per run: tests compare the paths in one process.
@@ -414,7 +414,13 @@ int dispatch_budget(const rasp::EpochArgs &a, const Plan &pl, const Device &dv, 
         constexpr int64_t UN = RASP_UNROLL_BIG;
         const int mode = refill_mode();
         int64_t k0 = 0;
-        if (mode == 2 && tau_max % UN == 0 && tau_max <= kRefillMaxTau) k0 = tau_max;
+        // auto: machine rows on 16-byte boundaries only (the paper rows' n = 250
+        // 32-bit words are not: refilled, 0.92-1.09 ms against 0.90-0.99 on
+        // epochs at tau 256-1024, and 1.24-1.49 with the aligned-only loader
+        // the refill kernel keeps -- scripts/refill_policy.py)
+        const bool rows16 = (reinterpret_cast<uintptr_t>(a.in.M) % 16 == 0) &&
+                            (uint64_t(a.g.n) * sizeof(S)) % 16 == 0;
+        if (mode == 2 && rows16 && tau_max % UN == 0 && tau_max <= kRefillMaxTau) k0 = tau_max;
         if (mode == 1) {
             k0 = (std::max<int64_t>(epoch, 1) + UN - 1) / UN * UN;
             if (k0 >= tau_max) k0 = tau_max / UN * UN;

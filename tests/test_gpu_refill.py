@@ -164,8 +164,9 @@ def test_refill_first_epoch_with_survivors(torch_mod, case):
 
 def test_refill_not_used_where_it_loses(torch_mod):
     """Auto mode runs the refill kernel only when it takes the whole budget in
-    one launch (tau a multiple of the block, at most 2048); longer budgets
-    keep the epochs (the paper row: 2.60 ms on epochs, 2.91+ refilled)."""
+    one launch (tau a multiple of the block, at most 2048) on 16-byte aligned
+    machine rows; longer budgets keep the epochs (the paper row: 2.21 ms on
+    epochs, 2.60+ refilled), and so do misaligned rows (n = 250 words)."""
     torch = torch_mod
     case = (32, 256, 32, 32, 3000, 4096, np.uint32, True, None)
     p, c0 = _inputs(case, seed=7)
@@ -177,7 +178,7 @@ def test_refill_not_used_where_it_loses(torch_mod):
         dev = torch.device("cuda:0")
         eng = get_engine(p, dev)
         eng.warm(4, True)
-        for tau, refilled in ((4096, False), (1024, True)):
+        for tau, refilled in ((4096, False), (1024, True), (1000, False)):
             arrays = {f: c0[f].astype(np.uint32) for f in FIELDS}
             arrays.update(status=np.zeros(3000, np.int8), steps=np.zeros(3000, np.int64),
                           tau_h=np.full(3000, -1, np.int64))
@@ -187,6 +188,17 @@ def test_refill_not_used_where_it_loses(torch_mod):
             eng.run(src, tau, 16, fresh=True)
             torch.cuda.synchronize()
             assert (_native.load().rasp_launch_count() - n0 == 1) == refilled, tau
+        # misaligned rows (n * 4 bytes not a multiple of 16): epochs at any budget
+        p2, c2 = _inputs((32, 250, 16, 16, 3000), seed=9)
+        eng2 = get_engine(p2, dev)
+        eng2.warm(4, True)
+        arrays = {f: c2[f].astype(np.uint32) for f in FIELDS}
+        src = DeviceBatch.from_arrays(arrays, p2, dev, word_bytes=4)
+        torch.cuda.synchronize()
+        n0 = _native.load().rasp_launch_count()
+        eng2.run(src, 1024, 16, fresh=True)
+        torch.cuda.synchronize()
+        assert _native.load().rasp_launch_count() - n0 > 1
     finally:
         if old is not None:
             os.environ["RASP_REFILL"] = old
