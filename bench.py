@@ -6,11 +6,11 @@ Workload (BASELINE.json configs[1]): per GPU, 2^20 synthetic
 programs from generator G (seed = rank), w=16, n=64, ell=8, s=8, run to halt
 with a 1024-step cap.  Each rank runs its own shard (weak scaling; no
 collective on the data path -- after the run the 102-bucket halting
-histogram, i.e. the halt counts, is all-reduced over NCCL and every shard's
-results stay on its GPU).  --config c3 is BASELINE configs[2]: 16M machines
-in total split across the ranks (strong scaling) with the output gather of
-that config: rank 0 gathers every shard's verdicts and output tapes over
-NCCL (--gather on|off overrides); c1 and c5 are configs[0] and configs[4].
+histogram, i.e. the halt counts, is all-reduced over NCCL and rank 0 gathers
+every shard's verdicts and output tapes; --gather off keeps the
+results on their GPUs).  --config c3 is BASELINE configs[2]: 16M machines in
+total split across the ranks (strong scaling), with the same collectives;
+c1 and c5 are configs[0] and configs[4].
 
 One "step" = one full run of the batch from c0 (out-of-place, c0 is never
 modified) with the halting histogram counted inside the run (rasp_run_hist).  Metric: machine-steps/s
