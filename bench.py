@@ -607,6 +607,8 @@ def bench_batch(args, world, rank, local_rank, dev):
     def run_step(st):   # the run with its halting histogram counted in the epoch kernels
         eng.run(src, tau, args.epoch, out=dst, fresh=True, stream=st, hist=hist)
 
+    recv = {}   # rank 0: gather receive buffers, reused by every step
+
     def collectives():
         """N > 1: halt counts all-reduced, verdicts + output tapes gathered to
         rank 0; host-staged under gloo."""
@@ -615,9 +617,11 @@ def bench_batch(args, world, rank, local_rank, dev):
         if gloo:
             hist.copy_(h)
         if do_gather:   # output tapes travel as bytes (no uint16 collectives in NCCL or gloo)
-            for t in (dst.status, dst.steps, dst.tau_h, dst.y.view(torch.uint8)):
+            for k, t in enumerate((dst.status, dst.steps, dst.tau_h, dst.y.view(torch.uint8))):
                 tt = t.cpu() if gloo else t
-                gather_to_root(tt, d_total, world, rank, sizes=sizes)
+                got = gather_to_root(tt, d_total, world, rank, sizes=sizes, out=recv.get(k))
+                if got is not None:   # rank 0 keeps its receive buffers across steps
+                    recv[k] = got._base if got._base is not None else got
 
     for _ in range(max(args.warmup, 0)):
         run_step(stream)

@@ -69,13 +69,16 @@ def reduce_histogram(hist: torch.Tensor, group=None) -> torch.Tensor:
     return hist
 
 
-def gather_to_root(t: torch.Tensor, d_total: int, world: int, rank: int, group=None, sizes=None):
+def gather_to_root(t: torch.Tensor, d_total: int, world: int, rank: int, group=None, sizes=None,
+                   out: torch.Tensor | None = None):
     """Gather contiguous shards of a per-machine tensor to rank 0.
 
     Shards may differ in length by the partition (`sizes`: machines per rank,
     default shard_bounds(d_total, world, k)); every rank pads to the largest
     shard so one collective moves everything.  Returns the full [d_total, ...]
-    tensor on rank 0, None elsewhere."""
+    tensor on rank 0, None elsewhere.  `out` (rank 0): a receive buffer of at
+    least world x largest-shard rows to reuse across calls; with equal shards
+    the result is a view of it (no concatenation)."""
     if not (dist.is_available() and dist.is_initialized()) or world == 1:
         return t
     if sizes is None:
@@ -86,10 +89,18 @@ def gather_to_root(t: torch.Tensor, d_total: int, world: int, rank: int, group=N
     else:
         pad = torch.zeros((per,) + tuple(t.shape[1:]), dtype=t.dtype, device=t.device)
         pad[: t.shape[0]] = t
-    parts = [torch.empty_like(pad) for _ in range(world)] if rank == 0 else None
+    parts = None
+    if rank == 0:
+        shape = (world * per,) + tuple(t.shape[1:])
+        if out is None or out.shape[0] < world * per or tuple(out.shape[1:]) != shape[1:] or \
+                out.dtype != t.dtype or out.device != t.device:
+            out = torch.empty(shape, dtype=t.dtype, device=t.device)
+        parts = list(out[: world * per].view((world, per) + shape[1:]).unbind(0))
     dist.gather(pad, parts, dst=0, group=group)
     if rank != 0:
         return None
+    if all(sz == per for sz in sizes):
+        return out[:d_total]
     return torch.cat([parts[k][: sizes[k]] for k in range(world)], 0)
 
 

@@ -87,3 +87,47 @@ def test_shard_bounds_partition():
                 assert b == c and a <= b
     with pytest.raises(ValueError):
         shard_bounds(10, 2, 2)
+
+
+def _reuse_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2604_12902_b200 import sharding
+        got = []
+        for sizes in ([5, 5, 5], [5, 4, 3], [5, 5, 5]):   # equal, ragged, equal again
+            d = sum(sizes)
+            lo = sum(sizes[:rank])
+            full = torch.arange(d * 3, dtype=torch.int64).reshape(d, 3)
+            buf = None
+            for rep in range(2):   # the receive buffer is reused on the second call
+                res = sharding.gather_to_root(full[lo:lo + sizes[rank]] + rep, d, world, rank, sizes=sizes, out=buf)
+                if rank == 0:
+                    ok = torch.equal(res, full + rep)
+                    buf = res._base if res._base is not None else res
+                    got.append((ok, sizes == [5, 5, 5] and rep == 1 and res.data_ptr() == buf.data_ptr()
+                                or sizes != [5, 5, 5] or rep == 0))
+                else:
+                    got.append((res is None, True))
+        q.put((rank, got))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gather_reuses_the_receive_buffer():
+    """gather_to_root(out=...): rank 0's receive buffer is reused across calls
+    (bench.py's per-step gathers), equal shards come back as a view of it,
+    ragged ones concatenated; every result equals the unsharded tensor."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_reuse_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    msgs = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    for r in range(world):
+        assert all(a and b for a, b in msgs[r]), (r, msgs[r])
