@@ -1573,7 +1573,7 @@ __global__ void __launch_bounds__(32, 8) refill_kernel(const EpochArgs A)
             A.out.tau_h[m] = halted ? tend : -1;
             if (A.hist) atomicAdd(&hist_s[!halted ? 101u : tend < 100 ? static_cast<uint32_t>(tend) : 100u], 1u);
         }
-        store_row<S, SC, 8>(static_cast<S *>(A.out.M) + m * n, n, reinterpret_cast<const SC *>(gb + lm));
+        store_row<S, SC, 16>(static_cast<S *>(A.out.M) + m * n, n, reinterpret_cast<const SC *>(gb + lm));
         // a parked machine: its true cell goes out after the row
         if (pk) static_cast<S *>(A.out.M)[m * n + ((pk - lm) >> SH)] = static_cast<S>(pkv);
         pk = 0;
