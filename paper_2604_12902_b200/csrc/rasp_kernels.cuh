@@ -372,8 +372,10 @@ __device__ __forceinline__ void load_rows_mu_aligned(const S *__restrict__ rm, u
 }
 
 // Shared loads in batches of B x 16 B before their global stores (one
-// shared-load latency per batch instead of one per 16 bytes: the refill
-// kernel's write-backs; the epoch kernel's measured +0.8% with B = 8).
+// shared-load latency per batch instead of one per 16 bytes).  Write-backs of
+// big tiles use B = 16: refill kernel C5 -1.4%, epoch kernel paper6 -0.8%,
+// paper +0.1% (B = 8 had measured +0.8% on the epoch kernel before rows
+// with a misaligned head were vectorised).
 template <class S, class SC, uint32_t B = 1>
 __device__ __forceinline__ void store_row(S *__restrict__ row, uint32_t ncells, const SC *col)
 {
@@ -1381,7 +1383,7 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
                 dst.steps[id] = steps0 + K;
             }
             if constexpr (!MX)
-                store_row<S, SC>(static_cast<S *>(dst.M) + id * n, n, reinterpret_cast<const SC *>(gb + lm));
+                store_row<S, SC, 16>(static_cast<S *>(dst.M) + id * n, n, reinterpret_cast<const SC *>(gb + lm));
         }
         if constexpr (MX)
             mx_store<S, SC, MB>(static_cast<S *>(A.out.M) + id * n, running, vecM, n, tile0, 0, lane,
