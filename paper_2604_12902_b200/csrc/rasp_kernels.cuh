@@ -1412,27 +1412,28 @@ epoch_kernel(const EpochArgs A, SC *gtiles)
 // the epoch ends, so a lane whose machine halted early idles: C5's first
 // epoch uses 41% of its lane-steps (p50 halting time 38 against a 320-step
 // epoch; 14% of the machines never halt, so nearly every tile runs it out).
-// For fresh runs whose budget is a multiple of the unrolled block, every
-// machine can start at a block boundary, so its budget also ends on one.
-// The kernel runs the first epoch of K0 steps (a multiple of the block): after
-// each block of UN steps a lane whose machine stopped moving (halted at its
-// move count, hv:115) or reached K0 (one more fetch decides: fixed there,
-// exhausted at K0 = tau_max, else a survivor for the epoch kernel's later
-// epochs, appended to the survivor list like theirs) is finished; its machine stays in place (a
-// fixed point, or parked: opcode 0 stored at its instruction cell, the true
-// value kept in a register).  Once at least `refill_min` lanes are free the
-// warp writes the finished machines back together and hands the free lanes
-// the next machines of its reservation: their rows are copied into the lanes'
-// columns asynchronously (4- or 8-byte cp.async; a TMA box cannot land in a
-// lane column) while the warp steps its other lanes for one more block, and
-// the new machines start at the next block boundary.  A lane whose column is
-// in flight (or that has no machine) steps on two zero cells after the
-// histogram (opcode 0 at i = 0: a fixed point that stores nothing).
-// Reservations are 32 consecutive machine ids claimed with one atomic, one
-// reservation ahead; each refill warms L2 with the rows of the next pf_dist
-// ids.  With K0 = tau_max one launch runs the whole budget.
-// cp.async row fills (4/8-byte copies) for the refill kernel: measured slower
-// (C5 2.06 against 1.65 ms: the copies crowd the steps' shared loads)
+// For fresh runs every machine can start at a block boundary, so with a
+// first epoch K0 that is a multiple of the unrolled block its budget also
+// ends on one.  The kernel runs that first epoch (by default the whole
+// budget): after each block of UN steps a lane whose machine stopped moving
+// (halted at its move count, hv:115) or reached K0 (one more fetch decides:
+// fixed there, exhausted at K0 = tau_max, else a survivor for the epoch
+// kernel's later epochs, appended to the survivor list like theirs) is
+// finished; its machine stays in place (a fixed point, or parked: opcode 0
+// stored at its instruction cell, the true value kept in a register and
+// written after the row).  Once at least `refill_min` lanes are free the warp
+// writes the finished machines back together (batches of 16 x 16 B shared
+// loads, then the stores) and the free lanes load the next machines of the
+// warp's reservation: the M row and a tape of <= 32 cells in two memory round
+// trips (load_rows_mu_aligned), the warp waiting for them.  Reservations are
+// 32 consecutive machine ids claimed with one atomic, one reservation ahead;
+// each refill warms L2 with the rows of the next pf_dist ids.  Lanes without a
+// machine step on two zero cells after the histogram (opcode 0 at i = 0: a
+// fixed point that stores nothing).
+// RASP_REFILL_ASYNC=1 (measured slower, C5 2.06 against 1.65 ms: the copies
+// crowd the steps' shared loads) copies the rows with 4- or 8-byte cp.async
+// instead (a TMA box cannot land in a lane column) while the warp steps its
+// other lanes for one more block, the loading lanes parked on the zero cells.
 #ifndef RASP_REFILL_ASYNC
 #define RASP_REFILL_ASYNC 0
 #endif
