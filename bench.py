@@ -765,6 +765,10 @@ def bench_batch(args, world, rank, local_rank, dev):
                      args.config, "synthetic (generator G, SURVEY §8d; seed = shard index)"),
         "config": cfg,
         "run": {"machines_per_gpu": d, "shards_rank0": [k for k, _ in shards], "epoch": args.epoch,
+                "kernels_per_step": launches_per_step,
+                "epoch_note": "first-epoch length passed to rasp_run; a fresh run of big machines "
+                              "(u32/u64 tiles) whose budget is a multiple of 16 and at most 2048, on "
+                              "16-byte aligned rows, runs as one refill_kernel launch instead (DESIGN.md §3)",
                 "machine_steps": total_steps, "halted_frac": total_halted / d_total,
                 "l2": "flushed between steps (256 MB write, outside the events)",
                 "launch": ("CUDA graph replay of rasp_run_hist (histogram fused)" if graph is not None else
