@@ -90,7 +90,10 @@ size_t rasp_workspace_bytes(const rasp_params *p, uint64_t d);
  *     EXHAUSTED (status 2): steps = tau_max, tau_h unchanged (-1 from run_batch)
  *     final config = Phi^steps(c);  machines entering with status != 0 are untouched.
  *   epoch   : length of the first on-device epoch (the reference's q); later
- *             epochs double it.  Performance knob only.
+ *             epochs double it.  Performance knob only: a fresh run of big
+ *             machines (u32/u64 tiles) whose budget is a multiple of 16 and at
+ *             most 2048, on 16-byte aligned rows, runs as one per-lane refill
+ *             launch over the whole budget instead (same results).
  *   workspace: device buffer of at least rasp_workspace_bytes(p, d) bytes.
  * Asynchronous on `stream` (may synchronise internally only when tau_max is
  * too large for a fixed epoch schedule, to poll the live count).  A machine
