@@ -119,8 +119,12 @@ __device__ __forceinline__ void check_smem(uint32_t, uint32_t) {}
 #ifndef RASP_BLOCK_WARPS
 #define RASP_BLOCK_WARPS 4
 #endif
+// 5 blocks of 4 warps: 20 warps per SM with up to 102 registers.  Measured
+// (C2 / C3): 10 blocks (40 warps, 48 registers) 0.549 / 7.46 ms, 8 -> 0.522 /
+// 7.31, 6 -> 0.515 / 7.31, 5 -> 0.506 / 7.30, 4 -> 0.534 / 7.64; 10 blocks of
+// 2 warps = 5 of 4.
 #ifndef RASP_MIN_BLOCKS
-#define RASP_MIN_BLOCKS 10
+#define RASP_MIN_BLOCKS 5
 #endif
 // Matrix-op row moves in flight per lane (16 B each) when loading a tile.
 #ifndef RASP_MX_BATCH
