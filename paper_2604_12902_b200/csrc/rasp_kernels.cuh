@@ -1734,8 +1734,14 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h)
     return h;
 }
 
+// resident 8-warp blocks per SM of the enumeration kernel (C4: 5 -> 0.896 s;
+// 4 / 3 / 2 -> 0.991 / 0.989 / 1.000 s: unlike the epoch kernel's small tiles,
+// this ALU-bound kernel wants its 40 warps)
+#ifndef RASP_ENUM_MIN_BLOCKS
+#define RASP_ENUM_MIN_BLOCKS 5
+#endif
 template <bool POW2, Arith AR, uint32_t UN>
-__global__ void __launch_bounds__(256, 5)
+__global__ void __launch_bounds__(256, RASP_ENUM_MIN_BLOCKS)
 enum_kernel(const EnumArgs A)
 {
     using SC = uint16_t;
