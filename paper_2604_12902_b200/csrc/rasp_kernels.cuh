@@ -1735,8 +1735,8 @@ __device__ __forceinline__ uint32_t fmix32(uint32_t h)
 }
 
 // resident 8-warp blocks per SM of the enumeration kernel (C4: 5 -> 0.896 s;
-// 4 / 3 / 2 -> 0.991 / 0.989 / 1.000 s: unlike the epoch kernel's small tiles,
-// this ALU-bound kernel wants its 40 warps)
+// 6 / 4 / 3 / 2 -> 0.941 / 0.991 / 0.989 / 1.000 s: unlike the epoch
+// kernel's small tiles, this ALU-bound kernel wants its 40 warps)
 #ifndef RASP_ENUM_MIN_BLOCKS
 #define RASP_ENUM_MIN_BLOCKS 5
 #endif
